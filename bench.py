@@ -1,0 +1,334 @@
+#!/usr/bin/env python
+"""DIGEST epoch benchmark on B200 (one partition per GPU).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config products]
+                    [--mode async|sync] [--impl ours|reference]
+
+A step is one full DIGEST training epoch (Alg. 1) of the products-shaped
+workload (BASELINE.json configs[4]) partitioned into M = N parts, one per GPU:
+pull (every N_sync epochs), L layer forwards with the boundary push, loss,
+backward, gradient allreduce and the optimizer step, all in libdigest.so.
+Prints ONE JSON line on rank 0.
+
+--impl reference times the CPU oracle (the base contract's reference arm for this
+tier) on the host cores, on a bounded sample of the same workload.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "epoch time (s) and SpMM GTEPS + HBM GB/s % of peak at 1/2/4/8 B200"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="products")
+    ap.add_argument("--mode", default="async", choices=["async", "sync"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--sample-frac", type=float, default=0.02,
+                    help="oracle sample: fraction of nodes/edges of the workload")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["hbm_gbs"], p.get("bf16_tflops"), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+# ---------------------------------------------------------------- clocks during the timed region
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu, self.proc, self.lines = gpu, None, []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- oracle (reference arm / cpu_baseline)
+def oracle_sample_epoch_seconds(cfg_name, M, frac, steps, warmup):
+    """Time oracle epochs on a products-shaped graph scaled to `frac` of the nodes and edges;
+    returns per-step seconds extrapolated to the full workload (time / frac)."""
+    from synth import get_config, make_inputs, make_block_parts
+    from synth.configs import scaled
+    import oracle
+    cfg = scaled(get_config(cfg_name), frac)
+    inp = make_inputs(cfg)
+    part = make_block_parts(cfg, M)
+    parts = [oracle.oracle_partition(inp.indptr, inp.indices, part, M, m) for m in range(M)]
+    times = []
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        oracle.oracle_train(inp.indptr, inp.indices, inp.x, inp.y, inp.train_mask, inp.weights,
+                            cfg.num_classes, part, M, sync_interval=get_config(cfg_name).sync_interval,
+                            epochs=1, parts=parts)
+        if i >= warmup:
+            times.append(time.perf_counter() - t0)
+    sample = (f"{steps} oracle epoch(s) of a {cfg_name}-shaped graph scaled to {frac:g} of the "
+              f"nodes/edges ({cfg.num_nodes} nodes, {cfg.nnz} nnz, dims {list(cfg.dims)}, M={M}); "
+              f"time x {1 / frac:g}")
+    return [t / frac for t in times], sample
+
+
+def cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def run_reference(a, rank, world):
+    if rank != 0:
+        return
+    per, sample = oracle_sample_epoch_seconds(a.config, world, a.sample_frac, a.steps, a.warmup)
+    v = float(np.mean(per))
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": a.config, "parts": world},
+            "cpu_baseline": {"value": v, "unit": "s", "cores": cores(), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU arm
+def run_ours(a, rank, world, local):
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2206_00057_b200 import capi as D
+    from paper_2206_00057_b200.engine import TrainConfig, build_workers
+    from synth import get_config, make_inputs, make_block_parts
+
+    cfg = get_config(a.config)
+    M = world
+    t0 = time.time()
+    inp = make_inputs(cfg)
+    part_of = make_block_parts(cfg, M)
+    t_gen = time.time() - t0
+
+    comm_grad = comm_halo = None
+    if world > 1:
+        ids = []
+        for _ in range(2):
+            uid = torch.zeros(128, dtype=torch.uint8)
+            if rank == 0:
+                uid = torch.tensor(list(D.digest_comm_unique_id()), dtype=torch.uint8)
+            uid = uid.cuda()
+            dist.broadcast(uid, 0)
+            ids.append(bytes(uid.cpu().tolist()))
+        comm_grad = D.digest_comm_init(ids[0], world, rank)
+        comm_halo = D.digest_comm_init(ids[1], world, rank)
+
+    tc = TrainConfig(dims=cfg.dims, num_classes=cfg.num_classes, sync_interval=cfg.sync_interval,
+                     lr=0.01, optimizer="adam", async_push=(a.mode == "async"))
+    t1 = time.time()
+    (w,) = build_workers(inp.indptr, inp.indices, inp.x, inp.y, inp.train_mask, inp.weights,
+                         part_of, M, tc, ranks=[rank], comm_grad=comm_grad, comm_halo=comm_halo)
+    torch.cuda.synchronize()
+    t_part = time.time() - t1
+    info = w.part.info
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    r = 0
+    for _ in range(a.warmup):
+        r += 1
+        w.epoch(r)
+    barrier()
+
+    # ---- timed region (device time, CUDA events on the launching stream)
+    clk = ClockSampler(local)
+    clk.start()
+    D.digest_prof_enable(True)
+    n0 = D.digest_launch_count()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(a.steps):
+        r += 1
+        w.epoch(r)
+    e1.record(stream)
+    barrier()
+    launches = D.digest_launch_count() - n0
+    ms = e0.elapsed_time(e1)
+    prof = D.digest_prof_read()
+    detail = D.digest_prof_detail()
+    D.digest_prof_enable(False)
+    clocks = clk.stop()
+    ms_max = max_over_ranks(ms)
+    step_s = ms_max / 1e3 / a.steps
+
+    # ---- e2e: same epochs through the public API with host inputs copied each step
+    e2e = None
+    if not a.no_e2e:
+        host = {k: getattr(w, k).cpu().pin_memory() for k in ("x_local", "labels", "train_mask")}
+        if w.x_halo is not None:
+            host["x_halo"] = w.x_halo.cpu().pin_memory()
+        loss_h = torch.zeros(1, dtype=torch.float64).pin_memory()
+        h2d = sum(t.numel() * t.element_size() for t in host.values())
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(a.steps):
+            r += 1
+            for k, t in host.items():
+                getattr(w, k).copy_(t, non_blocking=True)
+            w.epoch(r)
+            loss_h.copy_(w.loss, non_blocking=True)
+        f1.record(stream)
+        barrier()
+        e2e_s = max_over_ranks(f0.elapsed_time(f1)) / 1e3 / a.steps
+        e2e = {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": 8}
+
+    # ---- roofline of the dominant kernel (the SpMM instantiation with the largest time)
+    hbm, bf16, src = peaks()
+    dom = max((d for d in detail if d["cls"] == "spmm"), key=lambda d: d["ms"], default=None)
+    roof = None
+    if dom and dom["ms"] > 0:
+        per_launch_bytes = dom["bytes"] / dom["launches"]
+        avg_s = dom["ms"] / 1e3 / dom["launches"]
+        ach = per_launch_bytes / avg_s / 1e9
+        roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                "traffic": traffic_from_profiles(dom["tag"]), "kernel": f"k_spmm width {dom['tag']}",
+                "peak_source": src, "launches": dom["launches"], "avg_ms": avg_s * 1e3,
+                "alg_bytes_per_launch": per_launch_bytes}
+    spmm = prof["spmm"]
+    nnz_per_s = None
+    gteps = None
+    if spmm["ms"] > 0:
+        # nonzeros traversed = flops / (2 * width), summed per launch in the detail table
+        nz = sum(d["flops"] / (2.0 * d["tag"]) for d in detail if d["cls"] == "spmm" and d["tag"])
+        gteps = nz / (spmm["ms"] / 1e3) / 1e9
+    cpu = None
+    if rank == 0:
+        per, sample = oracle_sample_epoch_seconds(a.config, M, a.sample_frac, 1, 1)
+        cpu = {"value": float(np.mean(per)), "unit": "s", "cores": cores(), "kind": "oracle",
+               "sample": sample}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": step_s, "unit": "s", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": a.config, "num_nodes": cfg.num_nodes, "nnz": cfg.nnz,
+                       "parts": M, "dims": list(cfg.dims), "sync_interval": cfg.sync_interval,
+                       "mode": a.mode, "n_local": info.n_local, "n_halo": info.n_halo,
+                       "nnz_local": info.nnz, "l2": "inputs larger than L2 (no flush needed)"},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+            "spmm_gteps_rank0": gteps,
+            "kernel_ms_per_step": {k: v["ms"] / a.steps for k, v in prof.items()},
+            "setup_s": {"generate": t_gen, "partition_and_setup": t_part},
+        }
+        print(json.dumps(line), flush=True)
+    w.close()
+    if world > 1:
+        D.digest_comm_destroy(comm_grad)
+        D.digest_comm_destroy(comm_halo)
+        dist.destroy_process_group()
+
+
+def traffic_from_profiles(tag):
+    """dram bytes per launch of the dominant SpMM from the committed ncu summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            t = json.load(f)
+        return t.get(f"spmm_w{tag}")
+    except Exception:
+        return None
+
+
+def main():
+    a = parse()
+    rank, world, local = dist_env()
+    if a.gpus != world and world > 1:
+        print(f"warning: --gpus {a.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    if a.impl == "reference":
+        run_reference(a, rank, world)
+    else:
+        run_ours(a, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,238 @@
+/*
+ * digest.h -- C ABI of libdigest.so, the B200 (sm_100a) hot path of DIGEST
+ * (arXiv 2206.00057): the per-subgraph GCN layer forward/backward over local and
+ * stale out-of-subgraph ("halo") neighbours, the partition build, the periodic
+ * boundary push into the stale store and the weight-gradient allreduce.
+ *
+ * Citations: P:n = PAPER.md line n (section / equation), S:n = SPEC.md line n.
+ *
+ * Conventions (apply to every call unless stated):
+ *  - Pointers are DEVICE memory unless the parameter name ends in `_h` (host).
+ *    The caller owns every numeric buffer; the library owns the opaque handles
+ *    (digest_part, digest_store, digest_comm) and the device memory inside them.
+ *  - Matrices are row-major fp32.  A leading dimension `ld*` is in floats and must
+ *    be a multiple of 4 (16-byte rows, float4 / TMA rule) and >= the row width;
+ *    device pointers of matrices must be 16-byte aligned.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    All work is enqueued on it; nothing but digest_partition and the *_info /
+ *    *_export calls synchronises the host.  fwd/bwd/push/pull/xent/allreduce/step
+ *    never allocate, so an epoch is CUDA-graph capturable (pull in COPY mode).
+ *  - Errors: argument checks run before anything is enqueued; a non-OK status
+ *    means nothing was launched.  digest_last_error() returns a thread-local text
+ *    for the last non-OK status.  DIGEST_E_CUDA / DIGEST_E_NCCL report runtime
+ *    failures (asynchronous device faults surface at the next sync).  No C++
+ *    exception or abort crosses this ABI.
+ */
+#ifndef DIGEST_H
+#define DIGEST_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  DIGEST_OK = 0,
+  DIGEST_E_INVALID = 1,     /* bad argument value (range, alignment, empty part, ...) */
+  DIGEST_E_SHAPE = 2,       /* dimension mismatch */
+  DIGEST_E_STATE = 3,       /* call out of protocol order (e.g. pull of an unpushed level) */
+  DIGEST_E_CUDA = 4,        /* CUDA runtime error */
+  DIGEST_E_NCCL = 5,        /* NCCL error */
+  DIGEST_E_NOMEM = 6,       /* device allocation failed */
+  DIGEST_E_UNSUPPORTED = 7  /* valid but not implemented on this build/device */
+} digest_status;
+
+#define DIGEST_MAX_PARTS 64
+
+const char* digest_last_error(void);
+/* Number of kernels this library has launched in this process (all streams). */
+uint64_t digest_launch_count(void);
+
+/* ------------------------------------------------------------------ profiling
+ * Live per-kernel-class timing with CUDA events recorded on the stream each
+ * kernel is launched on.  Classes: 0 spmm, 1 gemm, 2 pack, 3 other.
+ * digest_prof_read synchronises on the recorded events and returns, per class,
+ * the summed milliseconds, the launch count and the algorithmic bytes/flops the
+ * launches declared (SURVEY §8.d.4 models). */
+enum { DIGEST_PROF_SPMM = 0, DIGEST_PROF_GEMM = 1, DIGEST_PROF_PACK = 2, DIGEST_PROF_OTHER = 3,
+       DIGEST_PROF_CLASSES = 4 };
+digest_status digest_prof_enable(int32_t on);
+digest_status digest_prof_read(double* ms_h, int64_t* launches_h, double* alg_bytes_h,
+                               double* alg_flops_h);
+/* The same, grouped by (class, tag) where tag is the SpMM width (0 for other
+ * kernels); writes up to max_groups groups and their count to *count_h. */
+digest_status digest_prof_read_detail(int32_t max_groups, int32_t* cls_h, int32_t* tag_h,
+                                      double* ms_h, int64_t* launches_h, double* alg_bytes_h,
+                                      double* alg_flops_h, int32_t* count_h);
+
+/* ------------------------------------------------------------------ communicator
+ * A library-owned NCCL communicator.  The 128-byte id is produced on rank 0 by
+ * digest_comm_unique_id and carried to the other ranks by the caller's process
+ * group (torch.distributed broadcast).  Used by the boundary exchange (C1) and the
+ * gradient allreduce (C2); the halo exchange gets its own side stream. */
+typedef struct digest_comm digest_comm;
+digest_status digest_comm_unique_id(uint8_t id_h[128]);
+digest_status digest_comm_init(const uint8_t id_h[128], int32_t nranks, int32_t rank,
+                               digest_comm** out_h);
+digest_status digest_comm_destroy(digest_comm* comm);
+
+/* ------------------------------------------------------------------ partition
+ * north_star call #1.  Builds, for partition `rank` of `num_parts`, the split of
+ * the GCN propagation matrix of Eq. 5 (P_m = P_in + P_out),
+ * the halo index (N(v)\V_m over v in V_m) and the boundary send lists.
+ *
+ *  indptr  int64[num_nodes+1], indices int32[nnz]: a symmetric adjacency, rows
+ *          sorted ascending, no duplicates, no self loops (checked: E_INVALID).
+ *  part_of int32[num_nodes] in [0, num_parts); every part non-empty.
+ *
+ * Result (bit-exact with the oracle):
+ *  local_ids : V_m ascending;  halo_ids : H_m ordered by (part_of, id);
+ *  extended column space [0, n_local) local, [n_local, n_local+n_halo) halo;
+ *  row i = loc(v) holds {(ext(u), P_vu) : u in N(v)} U {(i, P_vv)} sorted by
+ *  column (in-block entries first); P_vu = fp32(1/sqrt(double(deg v+1)*double(deg u+1)))
+ *  with global degrees (Kipf normalisation, "following GCN's definition").
+ *  send list to k: {u in V_m : N(u) meets V_k} ascending, concatenated over k;
+ *  recv_count[k] = #{u in H_m : part_of[u] = k}; offsets are exclusive prefixes.
+ *  The reverse-halo CSR (P_out^T: halo row j -> local columns) is always built.
+ * Synchronises `stream` (sizes are data-dependent).  The input arrays may be
+ * freed after return. */
+typedef struct digest_part digest_part;
+typedef struct {
+  int64_t num_nodes, n_local, n_halo, nnz, nnz_in, n_send, rh_nnz;
+  int32_t num_parts, rank;
+  int64_t send_count[DIGEST_MAX_PARTS], send_off[DIGEST_MAX_PARTS];
+  int64_t recv_count[DIGEST_MAX_PARTS], recv_off[DIGEST_MAX_PARTS];
+} digest_part_info;
+
+digest_status digest_partition(int64_t num_nodes, int64_t nnz, const int64_t* indptr,
+                               const int32_t* indices, const int32_t* part_of,
+                               int32_t num_parts, int32_t rank, uint32_t flags,
+                               void* stream, digest_part** out_h);
+digest_status digest_part_get_info(const digest_part* part, digest_part_info* info_h);
+/* Copies the partition arrays into caller buffers (device); any NULL is skipped.
+ * Sizes: local_ids[n_local], halo_ids[n_halo], row_ptr[n_local+1], col/val[nnz],
+ * send_idx[n_send], rh_ptr[n_halo+1], rh_col/rh_val[rh_nnz]. */
+digest_status digest_part_export(const digest_part* part, int32_t* local_ids,
+                                 int32_t* halo_ids, int64_t* row_ptr, int32_t* col,
+                                 float* val, int32_t* send_idx, int64_t* rh_ptr,
+                                 int32_t* rh_col, float* rh_val, void* stream);
+digest_status digest_part_destroy(digest_part* part);
+
+/* ------------------------------------------------------------------ stale store
+ * The stale representation store H~^(l), l in [1, L-1] (levels never
+ * equal L).  Per level: a front buffer (read by the layer that
+ * consumes level l) and a back buffer (written by pushes), each n_halo x ld_l
+ * with ld_l = round_up(width_l, 4), zero at creation (cold start).
+ * comm == NULL: single-process store; several stores of one process (the M
+ * partitions of a loopback run) are linked with digest_store_link so a push
+ * writes straight into the peers' back buffers (a fused gather + put). */
+typedef struct digest_store digest_store;
+enum { DIGEST_PUSH_ASYNC = 1u, DIGEST_PUSH_L2NORM = 2u };
+enum { DIGEST_PULL_FLIP = 0, DIGEST_PULL_COPY = 1 };
+
+digest_status digest_store_create(const digest_part* part, digest_comm* comm,
+                                  int32_t num_levels, const int32_t* width_h,
+                                  digest_store** out_h);
+/* Link the stores of all partitions of one process, index = rank (loopback). */
+digest_status digest_store_link(digest_store* const* stores_h, int32_t count);
+/* north_star call #4 ("push", Alg. 1 PUSH P:220-221).  Packs the boundary
+ * rows H_local[send_idx] of level `level` (optionally row-L2-normalised, Alg. 1
+ * P:226) and delivers them into every peer's back buffer at the
+ * (owner, id) segment of its halo.  `version` = epoch r.  With DIGEST_PUSH_ASYNC
+ * the exchange runs on the store's side stream behind an event (overlap with the
+ * next layer).  Collective: every rank pushes the same (level, version). */
+digest_status digest_push_boundary(digest_store* store, int32_t level, const float* H_local,
+                                   int64_t ld, int64_t version, uint32_t flags,
+                                   void* stream);
+/* Alg. 1 PULL: make the last pushed version of `level` the front
+ * buffer.  Requires the back version < epoch (pushes become visible only to later
+ * epochs); if no push happened since the last pull this is a no-op.  Mode FLIP
+ * swaps pointers; COPY copies back -> a fixed front (graph-safe).  Makes `stream`
+ * wait for an in-flight async exchange.  *front_h receives the front pointer. */
+digest_status digest_pull(digest_store* store, int32_t level, int64_t epoch, int32_t mode,
+                          void* stream, const float** front_h);
+/* Row gather dst[i, 0:width] = src[idx[i], 0:width], i < n (e.g. the static layer-1
+ * inputs X[V_m] and X[H_m] of X_ext^(0)).  width % 4 == 0. */
+digest_status digest_gather_rows(const float* src, int64_t ld_src, const int32_t* idx, int64_t n,
+                                 float* dst, int64_t ld_dst, int32_t width, void* stream);
+/* Current front buffer, its leading dimension and the version it holds. */
+digest_status digest_store_front(const digest_store* store, int32_t level,
+                                 const float** front_h, int64_t* ld_h, int64_t* version_h);
+digest_status digest_store_destroy(digest_store* store);
+
+/* ------------------------------------------------------------------ one GCN layer
+ * north_star calls #2/#3.  Eq. 5: H = sigma(P_in X_in W + P_out X~_out W)
+ * and Eq. 6 / P:783-794 backward with the halo block constant.
+ * X_local: n_local x d_in (ld_x); X_halo: n_halo x d_in (ld_xh; NULL iff n_halo==0);
+ * W: d_in x d_out row-major (ld = d_out).
+ * order: AGG_FIRST computes A = P_m X_ext then Z = A W; XFORM_FIRST computes
+ * T = X_ext W then Z = P_m T; AUTO picks AGG_FIRST iff d_in <= d_out (the SpMM runs
+ * at width min(d_in, d_out)).  act RELU: H = max(Z, 0); NONE: H = Z (output layer).
+ * `saved` (size from digest_layer_workspace) keeps what backward needs (A for
+ * AGG_FIRST); the caller keeps X_local/X_halo and H_out alive until backward.
+ * scratch is per-call temporary memory. */
+typedef enum { DIGEST_ACT_NONE = 0, DIGEST_ACT_RELU = 1 } digest_act;
+typedef enum { DIGEST_ORDER_AUTO = 0, DIGEST_ORDER_AGG_FIRST = 1,
+               DIGEST_ORDER_XFORM_FIRST = 2 } digest_order;
+
+digest_status digest_layer_workspace(const digest_part* part, int32_t d_in, int32_t d_out,
+                                     int32_t order, size_t* saved_bytes_h,
+                                     size_t* scratch_bytes_h);
+digest_status digest_layer_fwd(const digest_part* part, const float* X_local, int64_t ld_x,
+                               const float* X_halo, int64_t ld_xh, const float* W,
+                               int32_t d_in, int32_t d_out, int32_t act, int32_t order,
+                               float* H_out, int64_t ld_h, void* saved, void* scratch,
+                               void* stream);
+/* G_out: n_local x d_out gradient of the layer output (ld_g).  H_out: the forward
+ * output (its sign is the ReLU mask, ReLU'(0) := 0); ignored for ACT_NONE.
+ * G_W (d_in x d_out, overwritten) = (P_m X_ext)^T D with D = G_out o sigma'(Z).
+ * G_in (n_local x d_in, ld_gi; NULL = skip, first layer) = P_in^T D W^T. */
+digest_status digest_layer_bwd(const digest_part* part, const float* X_local, int64_t ld_x,
+                               const float* X_halo, int64_t ld_xh, const float* W,
+                               int32_t d_in, int32_t d_out, int32_t act, int32_t order,
+                               const void* saved, const float* H_out, int64_t ld_h,
+                               const float* G_out, int64_t ld_g, float* G_W, float* G_in,
+                               int64_t ld_gi, void* scratch, void* stream);
+
+/* ------------------------------------------------------------------ loss
+ * Eq. 3 on training rows: for v with train_mask[v] != 0,
+ * l_v = logsumexp(z_v[0:C]) - z_v[y_v]; G_logits[v,0:C] = w_loss*(softmax - e_y),
+ * 0 on other rows and on padded columns >= C.  loss_out[0] (device double) =
+ * w_loss * sum_v l_v, reduced in a fixed order (deterministic).  scratch: see
+ * digest_xent_workspace. */
+digest_status digest_xent_workspace(int64_t n, size_t* scratch_bytes_h);
+digest_status digest_xent(const float* logits, int64_t n, int32_t C, int64_t ld,
+                          const int32_t* labels, const uint8_t* train_mask, float w_loss,
+                          float* G_logits, int64_t ld_g, double* loss_out, void* scratch,
+                          void* stream);
+
+/* ------------------------------------------------------------------ AGG and update
+ * north_star call #5 (Alg. 1 AGG; update rule P:896): grads <- scale *
+ * sum over ranks of grads, in place (ncclAllReduce sum, then a scale kernel).
+ * comm == NULL or a 1-rank comm: only the scale is applied. */
+digest_status digest_grad_allreduce(digest_comm* comm, float* grads, int64_t count,
+                                    float scale, void* stream);
+/* Loopback AGG for M partitions of one process: every buffer receives
+ * scale * (bufs[0] + ... + bufs[n-1]) summed in index order. */
+digest_status digest_grad_allreduce_local(float* const* bufs_h, int32_t n, int64_t count,
+                                          float scale, void* stream);
+/* Alg. 1 local update W <- W - lr*G. */
+digest_status digest_sgd_step(float* W, const float* G, int64_t count, float lr, void* stream);
+/* Adam, bias-corrected, step >= 1. */
+digest_status digest_adam_step(float* W, const float* G, float* m, float* v, int64_t count,
+                               float lr, float b1, float b2, float eps, int64_t step,
+                               void* stream);
+
+/* ------------------------------------------------------------------ dense helper
+ * C[M x N] = op(A[M x K] B[K x N]) in fp32 on the path the layer uses (exposed for
+ * tests and the GEMM roofline).  flags bit0: ReLU epilogue. */
+digest_status digest_gemm(const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
+                          int64_t ldc, int64_t M, int32_t N, int32_t K, uint32_t flags,
+                          void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DIGEST_H */

@@ -1,0 +1,299 @@
+"""Thin ctypes binding of include/digest.h (argument marshalling only).
+
+Every function here has the C name of the call it wraps, converts torch tensors to
+device pointers, checks the status and raises DigestError with the library's
+message.  All computation happens in libdigest.so; there is no Python or CPU
+fallback: importing this module fails loudly if the library is missing.
+"""
+import ctypes as C
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdigest.so")
+
+DIGEST_MAX_PARTS = 64
+ACT_NONE, ACT_RELU = 0, 1
+ORDER_AUTO, ORDER_AGG_FIRST, ORDER_XFORM_FIRST = 0, 1, 2
+PUSH_ASYNC, PUSH_L2NORM = 1, 2
+PULL_FLIP, PULL_COPY = 0, 1
+PROF_SPMM, PROF_GEMM, PROF_PACK, PROF_OTHER = 0, 1, 2, 3
+STATUS = {0: "OK", 1: "E_INVALID", 2: "E_SHAPE", 3: "E_STATE", 4: "E_CUDA", 5: "E_NCCL",
+          6: "E_NOMEM", 7: "E_UNSUPPORTED"}
+
+
+class DigestError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"digest {STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2206_00057_b200.build` "
+                      "(there is no CPU fallback)")
+lib = C.CDLL(LIB_PATH)
+
+_p, _i32, _i64, _u32, _f32, _sz = C.c_void_p, C.c_int32, C.c_int64, C.c_uint32, C.c_float, C.c_size_t
+
+
+class PartInfo(C.Structure):
+    _fields_ = [("num_nodes", _i64), ("n_local", _i64), ("n_halo", _i64), ("nnz", _i64),
+                ("nnz_in", _i64), ("n_send", _i64), ("rh_nnz", _i64), ("num_parts", _i32),
+                ("rank", _i32), ("send_count", _i64 * DIGEST_MAX_PARTS),
+                ("send_off", _i64 * DIGEST_MAX_PARTS), ("recv_count", _i64 * DIGEST_MAX_PARTS),
+                ("recv_off", _i64 * DIGEST_MAX_PARTS)]
+
+
+_SIGS = {
+    "digest_last_error": ([], C.c_char_p),
+    "digest_launch_count": ([], C.c_uint64),
+    "digest_prof_enable": ([_i32], _i32),
+    "digest_prof_read": ([_p, _p, _p, _p], _i32),
+    "digest_prof_read_detail": ([_i32, _p, _p, _p, _p, _p, _p, _p], _i32),
+    "digest_comm_unique_id": ([_p], _i32),
+    "digest_comm_init": ([_p, _i32, _i32, _p], _i32),
+    "digest_comm_destroy": ([_p], _i32),
+    "digest_partition": ([_i64, _i64, _p, _p, _p, _i32, _i32, _u32, _p, _p], _i32),
+    "digest_part_get_info": ([_p, _p], _i32),
+    "digest_part_export": ([_p] * 11, _i32),
+    "digest_part_destroy": ([_p], _i32),
+    "digest_store_create": ([_p, _p, _i32, _p, _p], _i32),
+    "digest_store_link": ([_p, _i32], _i32),
+    "digest_push_boundary": ([_p, _i32, _p, _i64, _i64, _u32, _p], _i32),
+    "digest_pull": ([_p, _i32, _i64, _i32, _p, _p], _i32),
+    "digest_gather_rows": ([_p, _i64, _p, _i64, _p, _i64, _i32, _p], _i32),
+    "digest_store_front": ([_p, _i32, _p, _p, _p], _i32),
+    "digest_store_destroy": ([_p], _i32),
+    "digest_layer_workspace": ([_p, _i32, _i32, _i32, _p, _p], _i32),
+    "digest_layer_fwd": ([_p, _p, _i64, _p, _i64, _p, _i32, _i32, _i32, _i32, _p, _i64, _p, _p, _p],
+                         _i32),
+    "digest_layer_bwd": ([_p, _p, _i64, _p, _i64, _p, _i32, _i32, _i32, _i32, _p, _p, _i64, _p, _i64,
+                          _p, _p, _i64, _p, _p], _i32),
+    "digest_xent_workspace": ([_i64, _p], _i32),
+    "digest_xent": ([_p, _i64, _i32, _i64, _p, _p, _f32, _p, _i64, _p, _p, _p], _i32),
+    "digest_grad_allreduce": ([_p, _p, _i64, _f32, _p], _i32),
+    "digest_grad_allreduce_local": ([_p, _i32, _i64, _f32, _p], _i32),
+    "digest_sgd_step": ([_p, _p, _i64, _f32, _p], _i32),
+    "digest_adam_step": ([_p, _p, _p, _p, _i64, _f32, _f32, _f32, _f32, _i64, _p], _i32),
+    "digest_gemm": ([_p, _i64, _p, _i64, _p, _i64, _i64, _i32, _i32, _u32, _p], _i32),
+}
+for _name, (_args, _res) in _SIGS.items():
+    _f = getattr(lib, _name)
+    _f.argtypes = _args
+    _f.restype = _res
+
+
+def _check(status):
+    if status != 0:
+        raise DigestError(status, lib.digest_last_error().decode(errors="replace"))
+
+
+def ptr(x):
+    """Device (or host) address of a tensor, an int, or None."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    if isinstance(x, torch.Tensor):
+        return x.data_ptr()
+    if isinstance(x, (C.c_void_p,)):
+        return x.value
+    raise TypeError(f"cannot take the address of {type(x)}")
+
+
+def stream_ptr(stream=None):
+    if stream is None:
+        if not torch.cuda.is_available():
+            return None
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def ld_of(t: torch.Tensor) -> int:
+    assert t.dim() == 2 and t.stride(1) == 1, "row-major 2-D tensor expected"
+    return t.stride(0)
+
+
+# ------------------------------------------------------------------ misc
+def digest_last_error() -> str:
+    return lib.digest_last_error().decode(errors="replace")
+
+
+def digest_launch_count() -> int:
+    return int(lib.digest_launch_count())
+
+
+def digest_prof_enable(on: bool):
+    _check(lib.digest_prof_enable(1 if on else 0))
+
+
+def digest_prof_read():
+    ms = (C.c_double * 4)()
+    n = (C.c_int64 * 4)()
+    b = (C.c_double * 4)()
+    f = (C.c_double * 4)()
+    _check(lib.digest_prof_read(ms, n, b, f))
+    names = ["spmm", "gemm", "pack", "other"]
+    return {names[i]: {"ms": ms[i], "launches": n[i], "bytes": b[i], "flops": f[i]} for i in range(4)}
+
+
+def digest_prof_read_detail(max_groups=64):
+    cls, tag = (C.c_int32 * max_groups)(), (C.c_int32 * max_groups)()
+    ms, b, f = (C.c_double * max_groups)(), (C.c_double * max_groups)(), (C.c_double * max_groups)()
+    n, cnt = (C.c_int64 * max_groups)(), C.c_int32()
+    _check(lib.digest_prof_read_detail(max_groups, cls, tag, ms, n, b, f, C.byref(cnt)))
+    names = ["spmm", "gemm", "pack", "other"]
+    return [{"cls": names[cls[i]], "tag": tag[i], "ms": ms[i], "launches": n[i], "bytes": b[i],
+             "flops": f[i]} for i in range(cnt.value)]
+
+
+digest_prof_detail = digest_prof_read_detail
+
+
+# ------------------------------------------------------------------ communicator
+def digest_comm_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _check(lib.digest_comm_unique_id(buf))
+    return bytes(buf)
+
+
+def digest_comm_init(uid: bytes, nranks: int, rank: int):
+    buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+    out = C.c_void_p()
+    _check(lib.digest_comm_init(buf, nranks, rank, C.byref(out)))
+    return out.value
+
+
+def digest_comm_destroy(comm):
+    _check(lib.digest_comm_destroy(comm))
+
+
+# ------------------------------------------------------------------ partition
+def digest_partition(num_nodes, nnz, indptr, indices, part_of, num_parts, rank, flags=0,
+                     stream=None):
+    out = C.c_void_p()
+    _check(lib.digest_partition(num_nodes, nnz, ptr(indptr), ptr(indices), ptr(part_of),
+                                num_parts, rank, flags, stream_ptr(stream), C.byref(out)))
+    return out.value
+
+
+def digest_part_get_info(part) -> PartInfo:
+    info = PartInfo()
+    _check(lib.digest_part_get_info(part, C.byref(info)))
+    return info
+
+
+def digest_part_export(part, local_ids=None, halo_ids=None, row_ptr=None, col=None, val=None,
+                       send_idx=None, rh_ptr=None, rh_col=None, rh_val=None, stream=None):
+    _check(lib.digest_part_export(part, ptr(local_ids), ptr(halo_ids), ptr(row_ptr), ptr(col),
+                                  ptr(val), ptr(send_idx), ptr(rh_ptr), ptr(rh_col), ptr(rh_val),
+                                  stream_ptr(stream)))
+
+
+def digest_part_destroy(part):
+    _check(lib.digest_part_destroy(part))
+
+
+# ------------------------------------------------------------------ store
+def digest_store_create(part, comm, widths):
+    arr = (C.c_int32 * max(1, len(widths)))(*widths)
+    out = C.c_void_p()
+    _check(lib.digest_store_create(part, comm, len(widths), arr, C.byref(out)))
+    return out.value
+
+
+def digest_store_link(stores):
+    arr = (C.c_void_p * len(stores))(*stores)
+    _check(lib.digest_store_link(arr, len(stores)))
+
+
+def digest_push_boundary(store, level, H_local, version, flags=0, stream=None):
+    _check(lib.digest_push_boundary(store, level, ptr(H_local), ld_of(H_local), version, flags,
+                                    stream_ptr(stream)))
+
+
+def digest_pull(store, level, epoch, mode=PULL_FLIP, stream=None) -> int:
+    out = C.c_void_p()
+    _check(lib.digest_pull(store, level, epoch, mode, stream_ptr(stream), C.byref(out)))
+    return out.value
+
+
+def digest_gather_rows(src, idx, dst, width=None, stream=None):
+    n = idx.numel()
+    _check(lib.digest_gather_rows(ptr(src), ld_of(src), ptr(idx), n, ptr(dst), ld_of(dst),
+                                  width or dst.shape[1], stream_ptr(stream)))
+
+
+def digest_store_front(store, level):
+    p, ld, ver = C.c_void_p(), C.c_int64(), C.c_int64()
+    _check(lib.digest_store_front(store, level, C.byref(p), C.byref(ld), C.byref(ver)))
+    return p.value, ld.value, ver.value
+
+
+def digest_store_destroy(store):
+    _check(lib.digest_store_destroy(store))
+
+
+# ------------------------------------------------------------------ layer
+def digest_layer_workspace(part, d_in, d_out, order=ORDER_AUTO):
+    s, t = C.c_size_t(), C.c_size_t()
+    _check(lib.digest_layer_workspace(part, d_in, d_out, order, C.byref(s), C.byref(t)))
+    return s.value, t.value
+
+
+def digest_layer_fwd(part, X_local, X_halo, ld_xh, W, d_in, d_out, act, order, H_out, saved,
+                     scratch, stream=None):
+    """X_halo may be a tensor, a raw device address (the store's front buffer) or None."""
+    _check(lib.digest_layer_fwd(part, ptr(X_local), ld_of(X_local), ptr(X_halo), ld_xh, ptr(W),
+                                d_in, d_out, act, order, ptr(H_out), ld_of(H_out), ptr(saved),
+                                ptr(scratch), stream_ptr(stream)))
+
+
+def digest_layer_bwd(part, X_local, X_halo, ld_xh, W, d_in, d_out, act, order, saved, H_out,
+                     G_out, G_W, G_in, scratch, stream=None):
+    _check(lib.digest_layer_bwd(part, ptr(X_local), ld_of(X_local), ptr(X_halo), ld_xh, ptr(W),
+                                d_in, d_out, act, order, ptr(saved), ptr(H_out),
+                                ld_of(H_out) if H_out is not None else 0, ptr(G_out),
+                                ld_of(G_out), ptr(G_W), ptr(G_in),
+                                ld_of(G_in) if G_in is not None else 0, ptr(scratch),
+                                stream_ptr(stream)))
+
+
+# ------------------------------------------------------------------ loss / AGG / update
+def digest_xent_workspace(n):
+    s = C.c_size_t()
+    _check(lib.digest_xent_workspace(n, C.byref(s)))
+    return s.value
+
+
+def digest_xent(logits, C_, labels, train_mask, w_loss, G_logits, loss_out, scratch, stream=None):
+    _check(lib.digest_xent(ptr(logits), logits.shape[0], C_, ld_of(logits), ptr(labels),
+                           ptr(train_mask), w_loss, ptr(G_logits), ld_of(G_logits), ptr(loss_out),
+                           ptr(scratch), stream_ptr(stream)))
+
+
+def digest_grad_allreduce(comm, grads, scale=1.0, stream=None):
+    _check(lib.digest_grad_allreduce(comm, ptr(grads), grads.numel(), scale, stream_ptr(stream)))
+
+
+def digest_grad_allreduce_local(bufs, scale=1.0, stream=None):
+    arr = (C.c_void_p * len(bufs))(*[ptr(b) for b in bufs])
+    _check(lib.digest_grad_allreduce_local(arr, len(bufs), bufs[0].numel(), scale,
+                                           stream_ptr(stream)))
+
+
+def digest_sgd_step(W, G, lr, stream=None):
+    _check(lib.digest_sgd_step(ptr(W), ptr(G), W.numel(), lr, stream_ptr(stream)))
+
+
+def digest_adam_step(W, G, m, v, lr, b1, b2, eps, step, stream=None):
+    _check(lib.digest_adam_step(ptr(W), ptr(G), ptr(m), ptr(v), W.numel(), lr, b1, b2, eps, step,
+                                stream_ptr(stream)))
+
+
+def digest_gemm(A, B, Cm, relu=False, stream=None):
+    M, K = A.shape
+    N = B.shape[1]
+    _check(lib.digest_gemm(ptr(A), ld_of(A), ptr(B), ld_of(B), ptr(Cm), ld_of(Cm), M, N, K,
+                           1 if relu else 0, stream_ptr(stream)))

@@ -1,0 +1,68 @@
+// Internal kernel entry points shared by the layer, store and ABI files.
+#pragma once
+#include "common.cuh"
+
+namespace dg {
+
+// Y[i, 0:w] = act( sum_{e in row i} val[e] * Xsrc(col[e])[0:w] ),
+// Xsrc(c) = X0 + c*ld0 if c < split else X1 + (c - split)*ld1.
+// row range of row i: [row_ptr[i], row_ptr[i] + in_len[i]) if in_len != NULL
+// (the in-block P_in part, whose entries come first), else [row_ptr[i], row_ptr[i+1]).
+struct SpmmArgs {
+  const int64_t* row_ptr;
+  const int32_t* in_len;
+  const int32_t* col;
+  const float* val;
+  int64_t n_rows;
+  int64_t nnz;   // entries the call traverses (for the byte model / GTEPS)
+  const float* X0;
+  int64_t ld0;
+  int64_t split;
+  const float* X1;
+  int64_t ld1;
+  float* Y;
+  int64_t ldy;
+  int32_t width;
+  int32_t relu;
+};
+digest_status spmm(const SpmmArgs& a, cudaStream_t s);
+
+// C = A * B (+ optional ReLU) with generic strides:
+//   A(i,k) = A[i*sAi + k*sAk],  B(k,j) = B[k*sBk + j*sBj],  C[i*ldc + j].
+struct GemmArgs {
+  const float* A;
+  int64_t sAi, sAk;
+  const float* B;
+  int64_t sBk, sBj;
+  float* C;
+  int64_t ldc;
+  int64_t M;
+  int32_t N;
+  int64_t K;
+  int32_t relu;
+};
+digest_status gemm(const GemmArgs& g, cudaStream_t s);        // dispatch (tensor core if eligible)
+digest_status gemm_simt(const GemmArgs& g, cudaStream_t s);   // CUDA-core fp32
+
+// Weight gradient over a very long K: C[M x N] (dense, ld = N) = sum over segments of
+// A_seg^T B_seg with A_seg [K_seg x M] (ld lda), B_seg [K_seg x N] (ld ldb).
+// Split-K with a fixed-order second pass (deterministic).  `mask` (optional, per
+// segment) multiplies B by 1[mask > 0] elementwise (ReLU' from the layer output).
+struct WgradSeg {
+  const float* A;
+  int64_t lda;
+  const float* B;
+  int64_t ldb;
+  const float* mask;
+  int64_t ldm;
+  int64_t K;
+};
+size_t wgrad_scratch_bytes(int64_t K_total, int32_t M, int32_t N);
+digest_status wgrad(const WgradSeg* segs, int nseg, int32_t M, int32_t N, float* C,
+                    void* scratch, cudaStream_t s);
+
+// D = G o 1[H > 0] (n x w)
+digest_status relu_mask(const float* G, int64_t ldg, const float* H, int64_t ldh, float* D,
+                        int64_t ldd, int64_t n, int32_t w, cudaStream_t s);
+
+}  // namespace dg

@@ -1,0 +1,261 @@
+// digest_layer_fwd / digest_layer_bwd: one GCN layer of DIGEST on partition m.
+//
+// Forward, Eq. 5:  H = sigma(P_in X_in W + P_out X~_out W) = sigma(P_m X_ext W)
+//   AGG_FIRST:   A = P_m X_ext (SpMM, width d_in)       -> saved
+//                H = sigma(A W) (GEMM + ReLU epilogue)
+//   XFORM_FIRST: T = X_ext W    (GEMM over n_local + n_halo rows, width d_out)
+//                H = sigma(P_m T) (SpMM + ReLU epilogue)
+// Backward, Eq. 6 and P:783-794, halo constant:
+//   D = G o 1[H > 0]
+//   AGG_FIRST:   G_W = A^T D;  G_in = P_in^T (D W^T) = P_in (D W^T)      (P_in symmetric)
+//   XFORM_FIRST: S_loc = P_in^T D = P_in D,  S_halo = P_out^T D (reverse-halo CSR)
+//                G_W = X_loc^T S_loc + X_halo^T S_halo;  G_in = S_loc W^T
+// P_in is the principal block P[V_m, V_m] of the symmetric P, so P_in^T = P_in and
+// the in-block part of each forward CSR row (its first in_len entries) serves the
+// transposed product without a second copy; only P_out^T needs the reverse CSR.
+#include "kernels.cuh"
+#include "part_internal.cuh"
+
+namespace dg {
+
+digest_status gemm(const GemmArgs& g, cudaStream_t s) { return gemm_simt(g, s); }
+
+}  // namespace dg
+
+namespace {
+
+using dg::round_up;
+
+struct Plan {
+  bool agg_first;
+  int64_t n, h;
+  int64_t ldi, ldo;   // padded widths of d_in / d_out scratch rows
+  size_t saved, scratch;
+};
+
+digest_status make_plan(const digest_part* p, int32_t d_in, int32_t d_out, int32_t order,
+                        Plan* pl) {
+  DG_ARG(p, DIGEST_E_INVALID, "NULL partition");
+  DG_ARG(d_in > 0 && d_out > 0, DIGEST_E_SHAPE, "d_in/d_out must be positive");
+  DG_ARG(d_in % 4 == 0 && d_out % 4 == 0, DIGEST_E_SHAPE,
+         "d_in (%d) and d_out (%d) must be multiples of 4 (pad features/classes)", d_in, d_out);
+  DG_ARG(order >= 0 && order <= 2, DIGEST_E_INVALID, "bad order");
+  pl->agg_first = order == DIGEST_ORDER_AUTO ? d_in <= d_out : order == DIGEST_ORDER_AGG_FIRST;
+  pl->n = p->n_local;
+  pl->h = p->n_halo;
+  pl->ldi = round_up(d_in, 4);
+  pl->ldo = round_up(d_out, 4);
+  const size_t f = sizeof(float);
+  size_t wg = dg::wgrad_scratch_bytes(pl->n + pl->h, d_in, d_out);
+  if (pl->agg_first) {
+    pl->saved = f * pl->n * pl->ldi;
+    size_t bwd = f * pl->n * pl->ldo + f * pl->n * pl->ldi + wg;
+    pl->scratch = bwd;
+  } else {
+    pl->saved = 0;
+    size_t fwd = f * (pl->n + pl->h) * pl->ldo;
+    size_t bwd = f * pl->n * pl->ldo + f * (pl->n + pl->h) * pl->ldo + wg;
+    pl->scratch = fwd > bwd ? fwd : bwd;
+  }
+  pl->saved = round_up(pl->saved, 256);
+  pl->scratch = round_up(pl->scratch, 256);
+  return DIGEST_OK;
+}
+
+digest_status check_mat(const void* p, int64_t ld, int32_t w, const char* name) {
+  DG_ARG(p, DIGEST_E_INVALID, "%s is NULL", name);
+  DG_ARG(ld >= w && ld % 4 == 0, DIGEST_E_INVALID, "%s: ld %lld must be >= %d and a multiple of 4",
+         name, (long long)ld, w);
+  DG_ARG(((uintptr_t)p & 15) == 0, DIGEST_E_INVALID, "%s must be 16-byte aligned", name);
+  return DIGEST_OK;
+}
+
+float* carve(void* base, size_t& off, size_t bytes) {
+  float* p = reinterpret_cast<float*>(reinterpret_cast<char*>(base) + off);
+  off += round_up(bytes, 256);
+  return p;
+}
+
+dg::SpmmArgs spmm_full(const digest_part* p, const float* X0, int64_t ld0, const float* X1,
+                       int64_t ld1, float* Y, int64_t ldy, int32_t w, int relu) {
+  dg::SpmmArgs a{};
+  a.row_ptr = p->row_ptr;
+  a.in_len = nullptr;
+  a.col = p->col;
+  a.val = p->val;
+  a.n_rows = p->n_local;
+  a.nnz = p->nnz;
+  a.X0 = X0;
+  a.ld0 = ld0;
+  a.split = p->n_local;
+  a.X1 = X1;
+  a.ld1 = ld1;
+  a.Y = Y;
+  a.ldy = ldy;
+  a.width = w;
+  a.relu = relu;
+  return a;
+}
+
+dg::SpmmArgs spmm_in(const digest_part* p, const float* X, int64_t ld, float* Y, int64_t ldy,
+                     int32_t w) {
+  dg::SpmmArgs a = spmm_full(p, X, ld, X, ld, Y, ldy, w, 0);
+  a.in_len = p->in_len;
+  a.nnz = p->nnz_in;
+  return a;
+}
+
+dg::GemmArgs gemm_rm(const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
+                     int64_t ldc, int64_t M, int32_t N, int64_t K, int relu) {
+  dg::GemmArgs g{};
+  g.A = A;
+  g.sAi = lda;
+  g.sAk = 1;
+  g.B = B;
+  g.sBk = ldb;
+  g.sBj = 1;
+  g.C = C;
+  g.ldc = ldc;
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.relu = relu;
+  return g;
+}
+
+}  // namespace
+
+extern "C" {
+
+digest_status digest_layer_workspace(const digest_part* part, int32_t d_in, int32_t d_out,
+                                     int32_t order, size_t* saved_bytes_h,
+                                     size_t* scratch_bytes_h) {
+  Plan pl;
+  DG_TRY(make_plan(part, d_in, d_out, order, &pl));
+  if (saved_bytes_h) *saved_bytes_h = pl.saved;
+  if (scratch_bytes_h) *scratch_bytes_h = pl.scratch;
+  return DIGEST_OK;
+}
+
+digest_status digest_layer_fwd(const digest_part* p, const float* X_local, int64_t ld_x,
+                               const float* X_halo, int64_t ld_xh, const float* W, int32_t d_in,
+                               int32_t d_out, int32_t act, int32_t order, float* H_out,
+                               int64_t ld_h, void* saved, void* scratch, void* stream) {
+  Plan pl;
+  DG_TRY(make_plan(p, d_in, d_out, order, &pl));
+  DG_ARG(act == DIGEST_ACT_NONE || act == DIGEST_ACT_RELU, DIGEST_E_INVALID, "bad act");
+  DG_TRY(check_mat(X_local, ld_x, d_in, "X_local"));
+  if (pl.h > 0) DG_TRY(check_mat(X_halo, ld_xh, d_in, "X_halo"));
+  DG_TRY(check_mat(H_out, ld_h, d_out, "H_out"));
+  DG_ARG(W, DIGEST_E_INVALID, "W is NULL");
+  DG_ARG(pl.saved == 0 || saved, DIGEST_E_INVALID, "saved is NULL");
+  DG_ARG(pl.agg_first || scratch, DIGEST_E_INVALID, "scratch is NULL");
+  cudaStream_t s = dg::as_stream(stream);
+  const int relu = act == DIGEST_ACT_RELU;
+  if (pl.agg_first) {
+    float* A = reinterpret_cast<float*>(saved);
+    DG_TRY(dg::spmm(spmm_full(p, X_local, ld_x, X_halo, ld_xh, A, pl.ldi, d_in, 0), s));
+    DG_TRY(dg::gemm(gemm_rm(A, pl.ldi, W, d_out, H_out, ld_h, pl.n, d_out, d_in, relu), s));
+  } else {
+    size_t off = 0;
+    float* T = carve(scratch, off, sizeof(float) * (pl.n + pl.h) * pl.ldo);
+    DG_TRY(dg::gemm(gemm_rm(X_local, ld_x, W, d_out, T, pl.ldo, pl.n, d_out, d_in, 0), s));
+    if (pl.h > 0)
+      DG_TRY(dg::gemm(gemm_rm(X_halo, ld_xh, W, d_out, T + pl.n * pl.ldo, pl.ldo, pl.h, d_out,
+                              d_in, 0), s));
+    DG_TRY(dg::spmm(spmm_full(p, T, pl.ldo, T + pl.n * pl.ldo, pl.ldo, H_out, ld_h, d_out, relu),
+                    s));
+  }
+  return DIGEST_OK;
+}
+
+digest_status digest_layer_bwd(const digest_part* p, const float* X_local, int64_t ld_x,
+                               const float* X_halo, int64_t ld_xh, const float* W, int32_t d_in,
+                               int32_t d_out, int32_t act, int32_t order, const void* saved,
+                               const float* H_out, int64_t ld_h, const float* G_out, int64_t ld_g,
+                               float* G_W, float* G_in, int64_t ld_gi, void* scratch,
+                               void* stream) {
+  Plan pl;
+  DG_TRY(make_plan(p, d_in, d_out, order, &pl));
+  DG_ARG(act == DIGEST_ACT_NONE || act == DIGEST_ACT_RELU, DIGEST_E_INVALID, "bad act");
+  DG_TRY(check_mat(G_out, ld_g, d_out, "G_out"));
+  if (act == DIGEST_ACT_RELU) DG_TRY(check_mat(H_out, ld_h, d_out, "H_out"));
+  if (G_in) DG_TRY(check_mat(G_in, ld_gi, d_in, "G_in"));
+  DG_ARG(W && G_W && scratch, DIGEST_E_INVALID, "W, G_W and scratch must be non-NULL");
+  cudaStream_t s = dg::as_stream(stream);
+  size_t off = 0;
+  // D = G o sigma'(Z)   (sigma'(Z) = 1[H > 0] for ReLU, ReLU'(0) := 0)
+  const float* D = G_out;
+  int64_t ldd = ld_g;
+  if (act == DIGEST_ACT_RELU) {
+    float* Dm = carve(scratch, off, sizeof(float) * pl.n * pl.ldo);
+    DG_TRY(dg::relu_mask(G_out, ld_g, H_out, ld_h, Dm, pl.ldo, pl.n, d_out, s));
+    D = Dm;
+    ldd = pl.ldo;
+  } else {
+    carve(scratch, off, sizeof(float) * pl.n * pl.ldo);
+  }
+  if (pl.agg_first) {
+    DG_ARG(saved, DIGEST_E_INVALID, "saved is NULL");
+    const float* A = reinterpret_cast<const float*>(saved);
+    float* U = carve(scratch, off, sizeof(float) * pl.n * pl.ldi);
+    void* wsc = carve(scratch, off, 0);
+    dg::WgradSeg seg{A, pl.ldi, D, ldd, nullptr, 0, pl.n};
+    DG_TRY(dg::wgrad(&seg, 1, d_in, d_out, G_W, wsc, s));
+    if (G_in) {
+      // U = D W^T : B(k, j) = W[j, k]
+      dg::GemmArgs g = gemm_rm(D, ldd, W, d_out, U, pl.ldi, pl.n, d_in, d_out, 0);
+      g.sBk = 1;
+      g.sBj = d_out;
+      DG_TRY(dg::gemm(g, s));
+      DG_TRY(dg::spmm(spmm_in(p, U, pl.ldi, G_in, ld_gi, d_in), s));
+    }
+  } else {
+    DG_TRY(check_mat(X_local, ld_x, d_in, "X_local"));
+    if (pl.h > 0) DG_TRY(check_mat(X_halo, ld_xh, d_in, "X_halo"));
+    float* S = carve(scratch, off, sizeof(float) * (pl.n + pl.h) * pl.ldo);
+    void* wsc = carve(scratch, off, 0);
+    DG_TRY(dg::spmm(spmm_in(p, D, ldd, S, pl.ldo, d_out), s));
+    if (pl.h > 0) {
+      dg::SpmmArgs a{};
+      a.row_ptr = p->rh_ptr;
+      a.in_len = nullptr;
+      a.col = p->rh_col;
+      a.val = p->rh_val;
+      a.n_rows = pl.h;
+      a.nnz = p->rh_nnz;
+      a.X0 = D;
+      a.ld0 = ldd;
+      a.split = INT64_MAX;
+      a.X1 = D;
+      a.ld1 = ldd;
+      a.Y = S + pl.n * pl.ldo;
+      a.ldy = pl.ldo;
+      a.width = d_out;
+      a.relu = 0;
+      DG_TRY(dg::spmm(a, s));
+    }
+    dg::WgradSeg segs[2] = {{X_local, ld_x, S, pl.ldo, nullptr, 0, pl.n},
+                            {X_halo, ld_xh, S + pl.n * pl.ldo, pl.ldo, nullptr, 0, pl.h}};
+    DG_TRY(dg::wgrad(segs, pl.h > 0 ? 2 : 1, d_in, d_out, G_W, wsc, s));
+    if (G_in) {
+      dg::GemmArgs g = gemm_rm(S, pl.ldo, W, d_out, G_in, ld_gi, pl.n, d_in, d_out, 0);
+      g.sBk = 1;
+      g.sBj = d_out;
+      DG_TRY(dg::gemm(g, s));
+    }
+  }
+  return DIGEST_OK;
+}
+
+digest_status digest_gemm(const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
+                          int64_t ldc, int64_t M, int32_t N, int32_t K, uint32_t flags,
+                          void* stream) {
+  DG_ARG(A && B && C, DIGEST_E_INVALID, "NULL matrix");
+  DG_ARG(M >= 0 && N > 0 && K > 0 && lda >= K && ldb >= N && ldc >= N, DIGEST_E_SHAPE,
+         "bad GEMM shape");
+  return dg::gemm(gemm_rm(A, lda, B, ldb, C, ldc, M, N, K, (int)(flags & 1u)),
+                  dg::as_stream(stream));
+}
+
+}  // extern "C"

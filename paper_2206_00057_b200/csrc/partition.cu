@@ -1,0 +1,505 @@
+// digest_partition: the per-rank split of the GCN propagation matrix (Eq. 5,
+// P:159-165), the halo index and the boundary send lists, built on
+// the device without sorting: every ordering the contract asks for is a stable
+// partition of an already-sorted sequence (rows sorted by id; loc() and the
+// per-owner halo rank are monotone in id), done with prefix sums and warp
+// match/ballot ranks.  One-time setup; not on the epoch path.
+#include <vector>
+
+#include "part_internal.cuh"
+#include "scan.cuh"
+
+namespace {
+
+using dg::ceil_div;
+
+constexpr int kWarpsPerBlock = 8;
+
+// P_vu = fp32(1/sqrt(double(deg v+1) * double(deg u+1)))  (reading A2; IEEE RN ops)
+__device__ __forceinline__ float prop_value(int64_t dv, int64_t du) {
+  double a = (double)(dv + 1), b = (double)(du + 1);
+  return __double2float_rn(__ddiv_rn(1.0, __dsqrt_rn(__dmul_rn(a, b))));
+}
+
+__global__ void k_validate(int64_t n, const int64_t* __restrict__ indptr,
+                           const int32_t* __restrict__ indices, const int32_t* __restrict__ part_of,
+                           int32_t M, int* __restrict__ part_cnt, int* __restrict__ bad) {
+  const int lane = threadIdx.x & 31;
+  int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = w; v < n; v += nw) {
+    int64_t beg = indptr[v], end = indptr[v + 1];
+    if (lane == 0) {
+      int p = part_of[v];
+      if (p < 0 || p >= M || end < beg) atomicOr(bad, 1);
+      else atomicAdd(&part_cnt[p], 1);
+    }
+    for (int64_t e = beg + lane; e < end; e += 32) {
+      int32_t u = indices[e];
+      if (u < 0 || u >= n || u == v) atomicOr(bad, 2);
+      else if (e + 1 < end && indices[e + 1] <= u) atomicOr(bad, 4);
+    }
+  }
+}
+
+__global__ void k_fill_local(int64_t n, const int32_t* __restrict__ part_of, int32_t rank,
+                             const int64_t* __restrict__ loc, int32_t* __restrict__ local_ids,
+                             int32_t* __restrict__ ext) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    if (part_of[v] == rank) {
+      local_ids[loc[v]] = (int32_t)v;
+      ext[v] = (int32_t)loc[v];
+    } else {
+      ext[v] = -1;
+    }
+  }
+}
+
+// halo_flag[u] = 1 for u outside V_m adjacent to V_m; owner bit mask per local row.
+__global__ void k_mark_halo(int64_t n_local, const int32_t* __restrict__ local_ids,
+                            const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                            const int32_t* __restrict__ part_of, int32_t rank,
+                            int32_t* __restrict__ halo_flag, unsigned long long* __restrict__ owners) {
+  const int lane = threadIdx.x & 31;
+  int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = w; i < n_local; i += nw) {
+    int32_t v = local_ids[i];
+    unsigned long long mask = 0;
+    for (int64_t e = indptr[v] + lane; e < indptr[v + 1]; e += 32) {
+      int32_t u = indices[e];
+      int p = part_of[u];
+      if (p != rank) {
+        halo_flag[u] = 1;
+        mask |= 1ull << p;
+      }
+    }
+    unsigned lo = __reduce_or_sync(0xffffffffu, (unsigned)(mask & 0xffffffffu));
+    unsigned hi = __reduce_or_sync(0xffffffffu, (unsigned)(mask >> 32));
+    if (lane == 0) owners[i] = ((unsigned long long)hi << 32) | lo;
+  }
+}
+
+struct IsLocal {
+  const int32_t* p;
+  int32_t r;
+  __device__ int32_t operator()(int64_t v) const { return p[v] == r; }
+};
+
+struct HaloOfOwner {
+  const int32_t* flag;
+  const int32_t* part_of;
+  int32_t k;
+  __device__ int32_t operator()(int64_t u) const { return flag[u] && part_of[u] == k; }
+};
+
+__global__ void k_fill_halo(int64_t n, const int32_t* __restrict__ flag,
+                            const int32_t* __restrict__ part_of, int32_t k, int64_t base,
+                            const int64_t* __restrict__ pos, int64_t n_local,
+                            int32_t* __restrict__ halo_ids, int32_t* __restrict__ ext) {
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    if (flag[u] && part_of[u] == k) {
+      int64_t j = base + pos[u];
+      halo_ids[j] = (int32_t)u;
+      ext[u] = (int32_t)(n_local + j);
+    }
+  }
+}
+
+struct RowLen {
+  const int32_t* ids;
+  const int64_t* indptr;
+  int32_t extra;
+  __device__ int64_t operator()(int64_t i) const {
+    int32_t v = ids[i];
+    return indptr[v + 1] - indptr[v] + extra;
+  }
+};
+
+// One warp per local row: write the row's entries sorted by extended column.
+// group(u) = 0 for local u (and the self loop), 1 + part_of[u] for halo u; ext is
+// increasing in (group, id), and each group is already id-sorted in the input row,
+// so the position of an entry is  start(group) + (#earlier entries of its group).
+__global__ void k_fill_rows(int64_t n_local, const int32_t* __restrict__ local_ids,
+                            const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                            const int32_t* __restrict__ part_of, const int32_t* __restrict__ ext,
+                            int32_t rank, int32_t M, const int64_t* __restrict__ row_ptr,
+                            int32_t* __restrict__ col, float* __restrict__ val,
+                            int32_t* __restrict__ in_len) {
+  extern __shared__ int smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  int* run = smem + wib * (DIGEST_MAX_PARTS + 1);
+  int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = w; i < n_local; i += nw) {
+    int32_t v = local_ids[i];
+    int64_t beg = indptr[v], end = indptr[v + 1];
+    int64_t dv = end - beg;
+    for (int g = lane; g <= M; g += 32) run[g] = 0;
+    __syncwarp();
+    int lt_self = 0;
+    for (int64_t e = beg + lane; e < end; e += 32) {
+      int32_t u = indices[e];
+      int p = part_of[u];
+      int g = p == rank ? 0 : p + 1;
+      atomicAdd(&run[g], 1);
+      lt_self += (g == 0 && u < v);
+    }
+    lt_self = __reduce_add_sync(0xffffffffu, lt_self);
+    __syncwarp();
+    if (lane == 0) {
+      in_len[i] = run[0] + 1;
+      int acc = 0;
+      for (int g = 0; g <= M; ++g) {
+        int c = run[g] + (g == 0 ? 1 : 0);
+        run[g] = acc;
+        acc += c;
+      }
+      int64_t o = row_ptr[i] + lt_self;
+      col[o] = (int32_t)i;
+      val[o] = prop_value(dv, dv);
+    }
+    __syncwarp();
+    for (int64_t e0 = beg; e0 < end; e0 += 32) {
+      int64_t e = e0 + lane;
+      bool act = e < end;
+      unsigned am = __ballot_sync(0xffffffffu, act);
+      if (act) {
+        int32_t u = indices[e];
+        int p = part_of[u];
+        int g = p == rank ? 0 : p + 1;
+        unsigned peers = __match_any_sync(am, g);
+        int r = __popc(peers & ((1u << lane) - 1u));
+        int pos = run[g] + r;
+        if (g == 0 && pos >= lt_self) pos += 1;
+        int64_t o = row_ptr[i] + pos;
+        col[o] = ext[u];
+        val[o] = prop_value(dv, indptr[u + 1] - indptr[u]);
+        __syncwarp(am);
+        if (r == 0) run[g] += __popc(peers);
+      }
+      __syncwarp();
+    }
+  }
+}
+
+struct SendTo {
+  const unsigned long long* owners;
+  int32_t k;
+  __device__ int32_t operator()(int64_t i) const { return (int32_t)((owners[i] >> k) & 1ull); }
+};
+
+__global__ void k_fill_send(int64_t n_local, const unsigned long long* __restrict__ owners,
+                            int32_t k, int64_t base, const int64_t* __restrict__ pos,
+                            int32_t* __restrict__ send_idx) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_local;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if ((owners[i] >> k) & 1ull) send_idx[base + pos[i]] = (int32_t)i;
+}
+
+struct LocalNbrCount {
+  const int32_t* halo_ids;
+  const int64_t* indptr;
+  const int32_t* indices;
+  const int32_t* part_of;
+  int32_t rank;
+  __device__ int64_t operator()(int64_t j) const {
+    int32_t u = halo_ids[j];
+    int64_t c = 0;
+    for (int64_t e = indptr[u]; e < indptr[u + 1]; ++e) c += part_of[indices[e]] == rank;
+    return c;
+  }
+};
+
+// One warp per halo row j: local neighbours of H_m[j] in ascending loc (= id) order.
+__global__ void k_fill_rh(int64_t n_halo, const int32_t* __restrict__ halo_ids,
+                          const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                          const int32_t* __restrict__ part_of, const int32_t* __restrict__ ext,
+                          int32_t rank, const int64_t* __restrict__ rh_ptr,
+                          int32_t* __restrict__ rh_col, float* __restrict__ rh_val) {
+  const int lane = threadIdx.x & 31;
+  int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t j = w; j < n_halo; j += nw) {
+    int32_t u = halo_ids[j];
+    int64_t beg = indptr[u], end = indptr[u + 1], du = end - beg;
+    int64_t o = rh_ptr[j];
+    for (int64_t e0 = beg; e0 < end; e0 += 32) {
+      int64_t e = e0 + lane;
+      int32_t x = e < end ? indices[e] : 0;
+      bool loc = e < end && part_of[x] == rank;
+      unsigned b = __ballot_sync(0xffffffffu, loc);
+      if (loc) {
+        int64_t q = o + __popc(b & ((1u << lane) - 1u));
+        rh_col[q] = ext[x];
+        rh_val[q] = prop_value(indptr[x + 1] - indptr[x], du);
+      }
+      o += __popc(b);
+    }
+  }
+}
+
+__global__ void k_count_lt(const int32_t* __restrict__ col, int64_t nnz, int64_t bound,
+                           unsigned long long* __restrict__ out) {
+  unsigned long long c = 0;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x)
+    c += col[e] < bound;
+  c = __reduce_add_sync(0xffffffffu, (unsigned)c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
+__global__ void k_max_row(const int64_t* __restrict__ ptr, int64_t n, unsigned long long* out) {
+  unsigned long long m = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, (unsigned long long)(ptr[i + 1] - ptr[i]));
+  atomicMax(out, m);
+}
+
+template <typename T>
+digest_status dmalloc(T** p, int64_t n) {
+  if (n <= 0) n = 1;
+  cudaError_t e = cudaMalloc((void**)p, sizeof(T) * (size_t)n);
+  if (e != cudaSuccess)
+    return dg::set_error(DIGEST_E_NOMEM, "cudaMalloc(%lld bytes): %s",
+                         (long long)(sizeof(T) * n), cudaGetErrorString(e));
+  return DIGEST_OK;
+}
+
+struct Temps {
+  std::vector<void*> ptrs;
+  ~Temps() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+  template <typename T>
+  digest_status alloc(T** p, int64_t n) {
+    DG_TRY(dmalloc(p, n));
+    ptrs.push_back(*p);
+    return DIGEST_OK;
+  }
+};
+
+void free_part(digest_part* p) {
+  if (!p) return;
+  cudaFree(p->local_ids);
+  cudaFree(p->halo_ids);
+  cudaFree(p->row_ptr);
+  cudaFree(p->col);
+  cudaFree(p->val);
+  cudaFree(p->in_len);
+  cudaFree(p->send_idx);
+  cudaFree(p->rh_ptr);
+  cudaFree(p->rh_col);
+  cudaFree(p->rh_val);
+  delete p;
+}
+
+digest_status build(int64_t N, int64_t nnz, const int64_t* indptr, const int32_t* indices,
+                    const int32_t* part_of, int32_t M, int32_t rank, cudaStream_t s,
+                    digest_part* P) {
+  Temps t;
+  const int grid = dg::num_sms() * 8, block = 256;
+  int* dcnt;
+  DG_TRY(t.alloc(&dcnt, M + 1));
+  DG_CUDA(cudaMemsetAsync(dcnt, 0, sizeof(int) * (M + 1), s));
+  DG_LAUNCH(DIGEST_PROF_OTHER, s, 0, 0, k_validate, grid, block, 0, N, indptr, indices, part_of,
+            M, dcnt, dcnt + M);
+  std::vector<int> hcnt(M + 1);
+  DG_CUDA(cudaMemcpyAsync(hcnt.data(), dcnt, sizeof(int) * (M + 1), cudaMemcpyDeviceToHost, s));
+  DG_CUDA(cudaStreamSynchronize(s));
+  if (hcnt[M] & 1) return dg::set_error(DIGEST_E_INVALID, "part_of out of [0, num_parts)");
+  if (hcnt[M] & 2) return dg::set_error(DIGEST_E_INVALID, "index out of range or self loop");
+  if (hcnt[M] & 4) return dg::set_error(DIGEST_E_INVALID, "adjacency rows not strictly sorted");
+  for (int k = 0; k < M; ++k)
+    if (hcnt[k] == 0) return dg::set_error(DIGEST_E_INVALID, "part %d is empty", k);
+
+  P->num_nodes = N;
+  P->num_parts = M;
+  P->rank = rank;
+  int64_t* tmp;
+  DG_TRY(t.alloc(&tmp, dg::scan_tmp_elems(N > nnz ? N : nnz) + 16));
+  int64_t* pos;  // generic int64 scratch of N+1
+  DG_TRY(t.alloc(&pos, N + 1));
+
+  // O2: V_m ascending, loc(v)
+  int64_t n_local = 0;
+  DG_TRY(dg::exclusive_scan(IsLocal{part_of, rank}, N, pos, tmp, s, &n_local));
+  P->n_local = n_local;
+  DG_TRY(dmalloc(&P->local_ids, n_local));
+  int32_t* ext;
+  DG_TRY(t.alloc(&ext, N));
+  DG_LAUNCH(DIGEST_PROF_OTHER, s, 0, 0, k_fill_local, grid, block, 0, N, part_of, rank, pos,
+            P->local_ids, ext);
+
+  // O3: halo flags, owner masks, halo ids ordered by (owner, id)
+  int32_t* flag;
+  DG_TRY(t.alloc(&flag, N));
+  DG_CUDA(cudaMemsetAsync(flag, 0, sizeof(int32_t) * N, s));
+  unsigned long long* owners;
+  DG_TRY(t.alloc(&owners, n_local));
+  DG_LAUNCH(DIGEST_PROF_OTHER, s, 0, 0, k_mark_halo, grid, block, 0, n_local, P->local_ids,
+            indptr, indices, part_of, rank, flag, owners);
+  P->recv_count.assign(M, 0);
+  P->recv_off.assign(M, 0);
+  int64_t h = 0;
+  std::vector<int64_t> hc(M, 0);
+  for (int k = 0; k < M; ++k) {
+    P->recv_off[k] = h;
+    if (k == rank) continue;
+    DG_TRY(dg::exclusive_scan(HaloOfOwner{flag, part_of, k}, N, pos, tmp, s, &hc[k]));
+    P->recv_count[k] = hc[k];
+    h += hc[k];
+  }
+  P->n_halo = h;
+  DG_TRY(dmalloc(&P->halo_ids, h));
+  // second sweep: fill halo ids in owner order (recompute each owner's ranks)
+  for (int k = 0; k < M; ++k) {
+    if (k == rank || hc[k] == 0) continue;
+    DG_TRY(dg::exclusive_scan(HaloOfOwner{flag, part_of, k}, N, pos, tmp, s, nullptr));
+    DG_LAUNCH(DIGEST_PROF_OTHER, s, 0, 0, k_fill_halo, grid, block, 0, N, flag, part_of, k,
+              P->recv_off[k], pos, n_local, P->halo_ids, ext);
+  }
+
+  // O4: local CSR
+  DG_TRY(dmalloc(&P->row_ptr, n_local + 1));
+  int64_t nnz_m = 0;
+  DG_TRY(dg::exclusive_scan(RowLen{P->local_ids, indptr, 1}, n_local, P->row_ptr, tmp, s, &nnz_m));
+  P->nnz = nnz_m;
+  DG_TRY(dmalloc(&P->col, nnz_m));
+  DG_TRY(dmalloc(&P->val, nnz_m));
+  DG_TRY(dmalloc(&P->in_len, n_local));
+  {
+    size_t sm = sizeof(int) * (DIGEST_MAX_PARTS + 1) * kWarpsPerBlock;
+    DG_LAUNCH(DIGEST_PROF_OTHER, s, 0, 0, k_fill_rows, grid, kWarpsPerBlock * 32, sm, n_local,
+              P->local_ids, indptr, indices, part_of, ext, rank, M, P->row_ptr, P->col, P->val,
+              P->in_len);
+  }
+
+  // O5: send lists
+  P->send_count.assign(M, 0);
+  P->send_off.assign(M, 0);
+  int64_t ns = 0;
+  for (int k = 0; k < M; ++k) {
+    P->send_off[k] = ns;
+    if (k == rank) continue;
+    DG_TRY(dg::exclusive_scan(SendTo{owners, k}, n_local, pos, tmp, s, &P->send_count[k]));
+    ns += P->send_count[k];
+  }
+  P->n_send = ns;
+  DG_TRY(dmalloc(&P->send_idx, ns));
+  for (int k = 0; k < M; ++k) {
+    if (k == rank || P->send_count[k] == 0) continue;
+    DG_TRY(dg::exclusive_scan(SendTo{owners, k}, n_local, pos, tmp, s, nullptr));
+    DG_LAUNCH(DIGEST_PROF_OTHER, s, 0, 0, k_fill_send, grid, block, 0, n_local, owners, k,
+              P->send_off[k], pos, P->send_idx);
+  }
+
+  // O6: reverse-halo CSR
+  DG_TRY(dmalloc(&P->rh_ptr, h + 1));
+  int64_t rh = 0;
+  DG_TRY(dg::exclusive_scan(LocalNbrCount{P->halo_ids, indptr, indices, part_of, rank}, h,
+                            P->rh_ptr, tmp, s, &rh));
+  P->rh_nnz = rh;
+  DG_TRY(dmalloc(&P->rh_col, rh));
+  DG_TRY(dmalloc(&P->rh_val, rh));
+  if (h > 0)
+    DG_LAUNCH(DIGEST_PROF_OTHER, s, 0, 0, k_fill_rh, grid, block, 0, h, P->halo_ids, indptr,
+              indices, part_of, ext, rank, P->rh_ptr, P->rh_col, P->rh_val);
+
+  // statistics used for kernel selection
+  unsigned long long* st;
+  DG_TRY(t.alloc(&st, 3));
+  DG_CUDA(cudaMemsetAsync(st, 0, sizeof(unsigned long long) * 3, s));
+  DG_LAUNCH(DIGEST_PROF_OTHER, s, 0, 0, k_count_lt, grid, block, 0, P->col, nnz_m,
+            (int64_t)n_local, st);
+  DG_LAUNCH(DIGEST_PROF_OTHER, s, 0, 0, k_max_row, grid, block, 0, P->row_ptr, n_local, st + 1);
+  if (h > 0)
+    DG_LAUNCH(DIGEST_PROF_OTHER, s, 0, 0, k_max_row, grid, block, 0, P->rh_ptr, h, st + 2);
+  unsigned long long hs[3];
+  DG_CUDA(cudaMemcpyAsync(hs, st, sizeof(hs), cudaMemcpyDeviceToHost, s));
+  DG_CUDA(cudaStreamSynchronize(s));
+  P->nnz_in = (int64_t)hs[0];
+  P->max_row = (int64_t)hs[1];
+  P->max_rh_row = (int64_t)hs[2];
+  return DIGEST_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+digest_status digest_partition(int64_t num_nodes, int64_t nnz, const int64_t* indptr,
+                               const int32_t* indices, const int32_t* part_of, int32_t num_parts,
+                               int32_t rank, uint32_t flags, void* stream, digest_part** out_h) {
+  (void)flags;
+  DG_ARG(out_h, DIGEST_E_INVALID, "out is NULL");
+  *out_h = nullptr;
+  DG_ARG(num_nodes > 0 && num_nodes < (1ll << 31), DIGEST_E_INVALID, "num_nodes out of range");
+  DG_ARG(nnz >= 0 && nnz < (1ll << 31), DIGEST_E_INVALID, "nnz out of range");
+  DG_ARG(indptr && part_of && (indices || nnz == 0), DIGEST_E_INVALID, "NULL input array");
+  DG_ARG(num_parts >= 1 && num_parts <= DIGEST_MAX_PARTS && num_parts <= num_nodes,
+         DIGEST_E_INVALID, "num_parts must be in [1, min(64, num_nodes)]");
+  DG_ARG(rank >= 0 && rank < num_parts, DIGEST_E_INVALID, "rank out of range");
+  digest_part* P = new digest_part();
+  digest_status st = build(num_nodes, nnz, indptr, indices, part_of, num_parts, rank,
+                           dg::as_stream(stream), P);
+  if (st != DIGEST_OK) {
+    free_part(P);
+    return st;
+  }
+  *out_h = P;
+  return DIGEST_OK;
+}
+
+digest_status digest_part_get_info(const digest_part* p, digest_part_info* info) {
+  DG_ARG(p && info, DIGEST_E_INVALID, "NULL argument");
+  *info = digest_part_info{};
+  info->num_nodes = p->num_nodes;
+  info->n_local = p->n_local;
+  info->n_halo = p->n_halo;
+  info->nnz = p->nnz;
+  info->nnz_in = p->nnz_in;
+  info->n_send = p->n_send;
+  info->rh_nnz = p->rh_nnz;
+  info->num_parts = p->num_parts;
+  info->rank = p->rank;
+  for (int k = 0; k < p->num_parts; ++k) {
+    info->send_count[k] = p->send_count[k];
+    info->send_off[k] = p->send_off[k];
+    info->recv_count[k] = p->recv_count[k];
+    info->recv_off[k] = p->recv_off[k];
+  }
+  return DIGEST_OK;
+}
+
+digest_status digest_part_export(const digest_part* p, int32_t* local_ids, int32_t* halo_ids,
+                                 int64_t* row_ptr, int32_t* col, float* val, int32_t* send_idx,
+                                 int64_t* rh_ptr, int32_t* rh_col, float* rh_val, void* stream) {
+  DG_ARG(p, DIGEST_E_INVALID, "NULL partition");
+  cudaStream_t s = dg::as_stream(stream);
+  auto cp = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
+    if (!dst || bytes == 0) return cudaSuccess;
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s);
+  };
+  DG_CUDA(cp(local_ids, p->local_ids, 4 * p->n_local));
+  DG_CUDA(cp(halo_ids, p->halo_ids, 4 * p->n_halo));
+  DG_CUDA(cp(row_ptr, p->row_ptr, 8 * (p->n_local + 1)));
+  DG_CUDA(cp(col, p->col, 4 * p->nnz));
+  DG_CUDA(cp(val, p->val, 4 * p->nnz));
+  DG_CUDA(cp(send_idx, p->send_idx, 4 * p->n_send));
+  DG_CUDA(cp(rh_ptr, p->rh_ptr, 8 * (p->n_halo + 1)));
+  DG_CUDA(cp(rh_col, p->rh_col, 4 * p->rh_nnz));
+  DG_CUDA(cp(rh_val, p->rh_val, 4 * p->rh_nnz));
+  DG_CUDA(cudaStreamSynchronize(s));
+  return DIGEST_OK;
+}
+
+digest_status digest_part_destroy(digest_part* p) {
+  free_part(p);
+  return DIGEST_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,336 @@
+// The stale representation store (Alg. 1 PULL/PUSH P:208-221).
+//
+// The paper keeps stale representations in a host shared-memory KVS (Plasma,
+// P:385).  On B200 every GPU's halo buffers ARE the store: level l of partition m
+// holds two n_halo x ld_l buffers (front = read by layer l+1, back = written by
+// pushes).  A push gathers the boundary rows H[send_idx] once and delivers them
+// into each peer's back buffer at the (owner, id) segment of that peer's halo —
+// which is exactly the sender's send order, so nothing is unpacked on receipt.
+//   * loopback (several partitions in one process): the gather kernel writes the
+//     peers' back buffers directly (fused gather + put);
+//   * NCCL: gather into a contiguous send buffer, then a grouped send/recv
+//     all-to-allv straight into the back buffers, optionally on a side stream
+//     (async mode, overlapping the next layer: P:250-251).
+// A pull flips front/back (or copies, CUDA-graph safe) only when the back buffer
+// holds a newer version that is older than the current epoch (reading A7).
+#include <vector>
+
+#include "comm_internal.cuh"
+#include "kernels.cuh"
+#include "part_internal.cuh"
+
+namespace {
+
+struct Level {
+  int32_t width = 0;
+  int64_t ld = 0;
+  float* buf[2] = {nullptr, nullptr};
+  int64_t ver[2] = {0, 0};
+  int front = 0;
+  float* send_buf = nullptr;
+  cudaEvent_t done = nullptr;   // exchange completion (async mode)
+  bool inflight = false;
+};
+
+struct Segs {
+  float* dst[DIGEST_MAX_PARTS];
+  int64_t start[DIGEST_MAX_PARTS + 1];  // send-row offsets per segment
+  int32_t nseg;
+};
+
+// Row s of the send list -> segment k (binary search), destination row s - start[k].
+// Optional row L2 normalisation (Alg. 1, applied to the pushed copies only).
+template <bool NORM>
+__global__ void k_pack(const float* __restrict__ H, int64_t ldh, const int32_t* __restrict__ idx,
+                       int64_t n_send, Segs segs, int64_t ld, int w4) {
+  const int lane = threadIdx.x & 31;
+  int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < n_send; r += nw) {
+    int lo = 0, hi = segs.nseg - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (segs.start[mid] <= r) lo = mid; else hi = mid - 1;
+    }
+    const float4* src = reinterpret_cast<const float4*>(H + (int64_t)idx[r] * ldh);
+    float4* dst = reinterpret_cast<float4*>(segs.dst[lo] + (r - segs.start[lo]) * ld);
+    float scale = 1.f;
+    if (NORM) {
+      float ss = 0.f;
+      for (int c = lane; c < w4; c += 32) {
+        float4 v = src[c];
+        ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      scale = ss > 0.f ? 1.f / sqrtf(ss) : 0.f;
+    }
+    for (int c = lane; c < w4; c += 32) {
+      float4 v = src[c];
+      if (NORM) {
+        v.x *= scale;
+        v.y *= scale;
+        v.z *= scale;
+        v.w *= scale;
+      }
+      dst[c] = v;
+    }
+  }
+}
+
+__global__ void k_copy(const float4* __restrict__ src, float4* __restrict__ dst, int64_t n4) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+}  // namespace
+
+struct digest_store {
+  const digest_part* part = nullptr;
+  digest_comm* comm = nullptr;
+  std::vector<Level> lev;
+  std::vector<digest_store*> peers;  // loopback group, index = rank
+  cudaStream_t side = nullptr;
+  cudaEvent_t packed = nullptr;
+};
+
+namespace {
+
+void destroy_store(digest_store* st) {
+  if (!st) return;
+  for (auto& L : st->lev) {
+    cudaFree(L.buf[0]);
+    cudaFree(L.buf[1]);
+    cudaFree(L.send_buf);
+    if (L.done) cudaEventDestroy(L.done);
+  }
+  if (st->packed) cudaEventDestroy(st->packed);
+  if (st->side) cudaStreamDestroy(st->side);
+  delete st;
+}
+
+digest_status get_level(digest_store* st, int32_t level, Level** out) {
+  DG_ARG(st, DIGEST_E_INVALID, "NULL store");
+  DG_ARG(level >= 1 && level <= (int32_t)st->lev.size(), DIGEST_E_INVALID,
+         "level %d outside [1, %d] (stale levels never equal L, P:208/P:220)", level,
+         (int)st->lev.size());
+  *out = &st->lev[level - 1];
+  return DIGEST_OK;
+}
+
+digest_status pack(const float* H, int64_t ldh, const int32_t* idx, int64_t n_send, const Segs& sg,
+                   int64_t ld, int32_t width, bool norm, cudaStream_t s) {
+  if (n_send == 0) return DIGEST_OK;
+  int64_t blocks = dg::ceil_div(n_send, 8);
+  int64_t cap = (int64_t)dg::num_sms() * 16;
+  if (blocks > cap) blocks = cap;
+  double bytes = (double)n_send * (8.0 * width + 4.0);
+  if (norm)
+    DG_LAUNCH(DIGEST_PROF_PACK, s, bytes, 0, k_pack<true>, (unsigned)blocks, 256, 0, H, ldh, idx,
+              n_send, sg, ld, width / 4);
+  else
+    DG_LAUNCH(DIGEST_PROF_PACK, s, bytes, 0, k_pack<false>, (unsigned)blocks, 256, 0, H, ldh, idx,
+              n_send, sg, ld, width / 4);
+  return DIGEST_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+digest_status digest_store_create(const digest_part* part, digest_comm* comm, int32_t num_levels,
+                                  const int32_t* width_h, digest_store** out_h) {
+  DG_ARG(part && out_h, DIGEST_E_INVALID, "NULL argument");
+  DG_ARG(num_levels >= 0 && num_levels <= 64 && (num_levels == 0 || width_h), DIGEST_E_INVALID,
+         "bad level list");
+  if (comm)
+    DG_ARG(comm->nranks == part->num_parts && comm->rank == part->rank, DIGEST_E_INVALID,
+           "communicator (%d ranks, rank %d) does not match the partition (%d parts, rank %d)",
+           comm->nranks, comm->rank, part->num_parts, part->rank);
+  *out_h = nullptr;
+  digest_store* st = new digest_store();
+  st->part = part;
+  st->comm = comm;
+  st->lev.resize(num_levels);
+  auto fail = [&](digest_status s) {
+    destroy_store(st);
+    return s;
+  };
+  for (int l = 0; l < num_levels; ++l) {
+    Level& L = st->lev[l];
+    if (width_h[l] <= 0 || width_h[l] % 4 != 0) {
+      destroy_store(st);
+      return dg::set_error(DIGEST_E_INVALID, "level width %d must be a positive multiple of 4",
+                           width_h[l]);
+    }
+    L.width = width_h[l];
+    L.ld = dg::round_up(L.width, 4);
+    size_t hb = sizeof(float) * (size_t)(part->n_halo > 0 ? part->n_halo : 1) * L.ld;
+    size_t sb = sizeof(float) * (size_t)(part->n_send > 0 ? part->n_send : 1) * L.ld;
+    for (int b = 0; b < 2; ++b) {
+      if (cudaMalloc(&L.buf[b], hb) != cudaSuccess)
+        return fail(dg::set_error(DIGEST_E_NOMEM, "halo buffer allocation failed"));
+      if (cudaMemset(L.buf[b], 0, hb) != cudaSuccess)
+        return fail(dg::set_error(DIGEST_E_CUDA, "cudaMemset failed"));
+    }
+    if (comm && comm->nranks > 1) {
+      if (cudaMalloc(&L.send_buf, sb) != cudaSuccess)
+        return fail(dg::set_error(DIGEST_E_NOMEM, "send buffer allocation failed"));
+    }
+    if (cudaEventCreateWithFlags(&L.done, cudaEventDisableTiming) != cudaSuccess)
+      return fail(dg::set_error(DIGEST_E_CUDA, "event creation failed"));
+  }
+  if (cudaStreamCreateWithFlags(&st->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&st->packed, cudaEventDisableTiming) != cudaSuccess)
+    return fail(dg::set_error(DIGEST_E_CUDA, "stream/event creation failed"));
+  *out_h = st;
+  return DIGEST_OK;
+}
+
+digest_status digest_store_link(digest_store* const* stores_h, int32_t count) {
+  DG_ARG(stores_h && count >= 1 && count <= DIGEST_MAX_PARTS, DIGEST_E_INVALID, "bad store list");
+  for (int i = 0; i < count; ++i) {
+    digest_store* s = stores_h[i];
+    DG_ARG(s, DIGEST_E_INVALID, "NULL store %d", i);
+    DG_ARG(s->part->num_parts == count && s->part->rank == i, DIGEST_E_INVALID,
+           "store %d belongs to partition %d of %d", i, s->part->rank, s->part->num_parts);
+    DG_ARG(!s->comm || s->comm->nranks == 1, DIGEST_E_INVALID, "linked stores must not use NCCL");
+    DG_ARG(s->lev.size() == stores_h[0]->lev.size(), DIGEST_E_INVALID, "level count mismatch");
+    for (size_t l = 0; l < s->lev.size(); ++l)
+      DG_ARG(s->lev[l].width == stores_h[0]->lev[l].width, DIGEST_E_INVALID, "width mismatch");
+  }
+  for (int i = 0; i < count; ++i) stores_h[i]->peers.assign(stores_h, stores_h + count);
+  return DIGEST_OK;
+}
+
+digest_status digest_push_boundary(digest_store* st, int32_t level, const float* H_local,
+                                   int64_t ld, int64_t version, uint32_t flags, void* stream) {
+  Level* L;
+  DG_TRY(get_level(st, level, &L));
+  const digest_part* p = st->part;
+  DG_ARG(H_local || p->n_local == 0, DIGEST_E_INVALID, "H_local is NULL");
+  DG_ARG(ld >= L->width && ld % 4 == 0 && ((uintptr_t)H_local & 15) == 0, DIGEST_E_INVALID,
+         "H_local: ld must be >= width and a multiple of 4, pointer 16-byte aligned");
+  DG_ARG(version > L->ver[0] && version > L->ver[1], DIGEST_E_STATE,
+         "push version %lld is not newer than the stored versions", (long long)version);
+  cudaStream_t s = dg::as_stream(stream);
+  const int M = p->num_parts, me = p->rank;
+  const int back = 1 - L->front;
+  const bool norm = (flags & DIGEST_PUSH_L2NORM) != 0;
+  const bool nccl = st->comm && st->comm->nranks > 1;
+  if (M > 1 && !nccl) {
+    DG_ARG((int)st->peers.size() == M, DIGEST_E_STATE,
+           "single-process store of a %d-part graph: link the stores first", M);
+    Segs sg{};
+    sg.nseg = M;
+    for (int k = 0; k < M; ++k) {
+      sg.start[k] = p->send_off[k];
+      if (k == me) {
+        sg.dst[k] = nullptr;
+        continue;
+      }
+      digest_store* pk = st->peers[k];
+      Level& Lk = pk->lev[level - 1];
+      sg.dst[k] = Lk.buf[1 - Lk.front] + pk->part->recv_off[me] * Lk.ld;
+    }
+    sg.start[M] = p->n_send;
+    DG_TRY(pack(H_local, ld, p->send_idx, p->n_send, sg, L->ld, L->width, norm, s));
+  } else if (nccl) {
+    if (L->inflight) DG_CUDA(cudaStreamWaitEvent(s, L->done, 0));  // send buffer reuse
+    Segs sg{};
+    sg.nseg = 1;
+    sg.dst[0] = L->send_buf;
+    sg.start[0] = 0;
+    sg.start[1] = p->n_send;
+    DG_TRY(pack(H_local, ld, p->send_idx, p->n_send, sg, L->ld, L->width, norm, s));
+    std::vector<const float*> sp(M);
+    std::vector<float*> rp(M);
+    std::vector<int64_t> cs(M), cr(M);
+    for (int k = 0; k < M; ++k) {
+      sp[k] = L->send_buf + p->send_off[k] * L->ld;
+      rp[k] = L->buf[back] + p->recv_off[k] * L->ld;
+      cs[k] = p->send_count[k] * L->ld;
+      cr[k] = p->recv_count[k] * L->ld;
+    }
+    cudaStream_t xs = s;
+    if (flags & DIGEST_PUSH_ASYNC) {
+      DG_CUDA(cudaEventRecord(st->packed, s));
+      DG_CUDA(cudaStreamWaitEvent(st->side, st->packed, 0));
+      xs = st->side;
+    }
+    DG_TRY(dg::comm_alltoallv(st->comm, sp.data(), cs.data(), rp.data(), cr.data(), xs));
+    DG_CUDA(cudaEventRecord(L->done, xs));
+    L->inflight = true;
+  }
+  L->ver[back] = version;
+  return DIGEST_OK;
+}
+
+digest_status digest_pull(digest_store* st, int32_t level, int64_t epoch, int32_t mode,
+                          void* stream, const float** front_h) {
+  Level* L;
+  DG_TRY(get_level(st, level, &L));
+  DG_ARG(mode == DIGEST_PULL_FLIP || mode == DIGEST_PULL_COPY, DIGEST_E_INVALID, "bad pull mode");
+  cudaStream_t s = dg::as_stream(stream);
+  const int back = 1 - L->front;
+  if (L->ver[back] >= epoch)
+    return dg::set_error(DIGEST_E_STATE,
+                         "pull at epoch %lld would expose version %lld (pushes are visible to "
+                         "later epochs only)", (long long)epoch, (long long)L->ver[back]);
+  if (L->ver[back] > L->ver[L->front]) {
+    if (L->inflight) {
+      DG_CUDA(cudaStreamWaitEvent(s, L->done, 0));
+      L->inflight = false;
+    }
+    if (mode == DIGEST_PULL_FLIP) {
+      L->front = back;
+    } else {
+      int64_t n4 = st->part->n_halo * L->ld / 4;
+      if (n4 > 0) {
+        int64_t blocks = dg::ceil_div(n4, 256);
+        int64_t cap = (int64_t)dg::num_sms() * 8;
+        DG_LAUNCH(DIGEST_PROF_PACK, s, 32.0 * n4, 0, k_copy, (unsigned)(blocks > cap ? cap : blocks),
+                  256, 0, reinterpret_cast<const float4*>(L->buf[back]),
+                  reinterpret_cast<float4*>(L->buf[L->front]), n4);
+      }
+      L->ver[L->front] = L->ver[back];
+    }
+  }
+  if (front_h) *front_h = L->buf[L->front];
+  return DIGEST_OK;
+}
+
+digest_status digest_gather_rows(const float* src, int64_t ld_src, const int32_t* idx, int64_t n,
+                                 float* dst, int64_t ld_dst, int32_t width, void* stream) {
+  DG_ARG(n >= 0 && width > 0 && width % 4 == 0 && ld_src >= width && ld_dst >= width &&
+             ld_src % 4 == 0 && ld_dst % 4 == 0,
+         DIGEST_E_SHAPE, "bad gather shape");
+  if (n == 0) return DIGEST_OK;
+  DG_ARG(src && idx && dst, DIGEST_E_INVALID, "NULL argument");
+  Segs sg{};
+  sg.nseg = 1;
+  sg.dst[0] = dst;
+  sg.start[0] = 0;
+  sg.start[1] = n;
+  return pack(src, ld_src, idx, n, sg, ld_dst, width, false, dg::as_stream(stream));
+}
+
+digest_status digest_store_front(const digest_store* st, int32_t level, const float** front_h,
+                                 int64_t* ld_h, int64_t* version_h) {
+  DG_ARG(st, DIGEST_E_INVALID, "NULL store");
+  DG_ARG(level >= 1 && level <= (int32_t)st->lev.size(), DIGEST_E_INVALID, "bad level");
+  const Level& L = st->lev[level - 1];
+  if (front_h) *front_h = L.buf[L.front];
+  if (ld_h) *ld_h = L.ld;
+  if (version_h) *version_h = L.ver[L.front];
+  return DIGEST_OK;
+}
+
+digest_status digest_store_destroy(digest_store* st) {
+  if (st && st->side) cudaStreamSynchronize(st->side);
+  destroy_store(st);
+  return DIGEST_OK;
+}
+
+}  // extern "C"

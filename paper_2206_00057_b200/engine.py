@@ -1,0 +1,236 @@
+"""The DIGEST epoch driver (host logic only; every step runs in libdigest.so).
+
+Implements Alg. 1 for one partition per worker:
+  * PULL  at the start of epoch r if r % N == 0, levels l in [1, L-1];
+  * layer l forward on [H^(l-1)_local ; front buffer of level l-1] (Eq. 5);
+  * PUSH  right after level l is computed if (r-1) % N == 0 and l < L;
+  * loss (Eq. 3), backward (Eq. 6), AGG as a gradient allreduce, update.
+Reading A7: all pulls of an epoch happen before any push of that epoch, so pulls
+only ever expose versions < r.  Torch provides memory, streams and process groups.
+
+Two deployments:
+  * DigestWorker with an NCCL communicator: one process per GPU (torchrun);
+  * LoopbackGroup: M partitions in one process on one GPU, stores linked so a push
+    writes the peers' back buffers directly (used by the single-GPU tests).
+"""
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import capi as D
+
+
+@dataclass
+class TrainConfig:
+    dims: tuple                 # (d_0, ..., d_L), padded (multiples of 4)
+    num_classes: int
+    sync_interval: int = 1
+    lr: float = 0.01
+    optimizer: str = "sgd"      # 'sgd' (parity) or 'adam' (the paper's)
+    order: int = D.ORDER_AUTO
+    async_push: bool = False
+    normalize_pushed: bool = False
+    pull_mode: int = D.PULL_FLIP
+
+
+class Partition:
+    """A digest_part handle plus its info (host copy)."""
+
+    def __init__(self, indptr, indices, part_of, num_parts, rank, stream=None):
+        n = indptr.numel() - 1
+        self.handle = D.digest_partition(n, indices.numel(), indptr, indices, part_of, num_parts,
+                                         rank, 0, stream)
+        self.info = D.digest_part_get_info(self.handle)
+        self.num_parts, self.rank = num_parts, rank
+        self.n_local, self.n_halo = self.info.n_local, self.info.n_halo
+
+    def export(self, device="cuda"):
+        i = self.info
+        t = lambda n, dt: torch.empty(max(n, 0), dtype=dt, device=device)
+        out = dict(local_ids=t(i.n_local, torch.int32), halo_ids=t(i.n_halo, torch.int32),
+                   row_ptr=t(i.n_local + 1, torch.int64), col=t(i.nnz, torch.int32),
+                   val=t(i.nnz, torch.float32), send_idx=t(i.n_send, torch.int32),
+                   rh_ptr=t(i.n_halo + 1, torch.int64), rh_col=t(i.rh_nnz, torch.int32),
+                   rh_val=t(i.rh_nnz, torch.float32))
+        D.digest_part_export(self.handle, **out)
+        M = self.num_parts
+        out.update(send_count=np.array(i.send_count[:M]), send_off=np.array(i.send_off[:M]),
+                   recv_count=np.array(i.recv_count[:M]), recv_off=np.array(i.recv_off[:M]))
+        return out
+
+    def close(self):
+        if self.handle:
+            D.digest_part_destroy(self.handle)
+            self.handle = None
+
+
+class DigestWorker:
+    """Training state of one partition on the current CUDA device."""
+
+    def __init__(self, part: Partition, cfg: TrainConfig, x_local, x_halo, labels, train_mask,
+                 weights, w_loss, comm_grad=None, comm_halo=None):
+        self.part, self.cfg = part, cfg
+        self.L = len(cfg.dims) - 1
+        dims = cfg.dims
+        dev = x_local.device
+        n, h = part.n_local, part.n_halo
+        self.x_local, self.x_halo = x_local, (x_halo if h > 0 else None)
+        self.labels, self.train_mask = labels, train_mask
+        self.w_loss = float(w_loss)
+        self.comm_grad, self.comm_halo = comm_grad, comm_halo
+        # weights: one flat buffer (AGG and the update are single launches)
+        sizes = [dims[l] * dims[l + 1] for l in range(self.L)]
+        self.W_flat = torch.empty(sum(sizes), dtype=torch.float32, device=dev)
+        self.G_flat = torch.zeros_like(self.W_flat)
+        self.W, self.GW, off = [], [], 0
+        for l, s in enumerate(sizes):
+            self.W.append(self.W_flat[off:off + s].view(dims[l], dims[l + 1]))
+            self.GW.append(self.G_flat[off:off + s].view(dims[l], dims[l + 1]))
+            off += s
+        for w, src in zip(self.W, weights):
+            w.copy_(torch.as_tensor(src, dtype=torch.float32))
+        self.adam_m = self.adam_v = None
+        if cfg.optimizer == "adam":
+            self.adam_m = torch.zeros_like(self.W_flat)
+            self.adam_v = torch.zeros_like(self.W_flat)
+        self.step_count = 0
+        # activations, saved state, gradients
+        self.H = [None] + [torch.empty(n, dims[l], device=dev) for l in range(1, self.L + 1)]
+        self.saved, scratch = [None], 0
+        for l in range(1, self.L + 1):
+            sv, sc = D.digest_layer_workspace(part.handle, dims[l - 1], dims[l], cfg.order)
+            self.saved.append(torch.empty(max(sv, 256), dtype=torch.uint8, device=dev))
+            scratch = max(scratch, sc)
+        self.scratch = torch.empty(max(scratch, 256), dtype=torch.uint8, device=dev)
+        self.G = [None] + [torch.empty(n, dims[l], device=dev) for l in range(1, self.L + 1)]
+        self.xent_scratch = torch.empty(max(D.digest_xent_workspace(n), 8), dtype=torch.uint8,
+                                        device=dev)
+        self.loss = torch.zeros(1, dtype=torch.float64, device=dev)
+        # stale store: levels 1..L-1 (never L)
+        self.store = D.digest_store_create(part.handle, comm_halo, list(dims[1:self.L]))
+        self.pulls = self.pushes = 0
+
+    # --------------------------------------------------------------- schedule pieces
+    def halo_input(self, l):
+        """(pointer, ld) of the halo rows feeding layer l."""
+        if l == 1:
+            return (self.x_halo, self.cfg.dims[0]) if self.x_halo is not None else (None, 0)
+        p, ld, _ = D.digest_store_front(self.store, l - 1)
+        return (p if self.part.n_halo > 0 else None), ld
+
+    def pull(self, epoch, stream=None):
+        for l in range(1, self.L):
+            D.digest_pull(self.store, l, epoch, self.cfg.pull_mode, stream)
+            self.pulls += 1
+
+    def forward(self, epoch, push: bool, stream=None):
+        dims, cfg = self.cfg.dims, self.cfg
+        flags = (D.PUSH_ASYNC if cfg.async_push else 0) | (D.PUSH_L2NORM if cfg.normalize_pushed else 0)
+        for l in range(1, self.L + 1):
+            xl = self.x_local if l == 1 else self.H[l - 1]
+            xh, ldh = self.halo_input(l)
+            act = D.ACT_RELU if l < self.L else D.ACT_NONE
+            D.digest_layer_fwd(self.part.handle, xl, xh, ldh, self.W[l - 1], dims[l - 1], dims[l],
+                               act, cfg.order, self.H[l], self.saved[l], self.scratch, stream)
+            if push and l < self.L:
+                D.digest_push_boundary(self.store, l, self.H[l], epoch, flags, stream)
+                self.pushes += 1
+
+    def loss_and_backward(self, stream=None):
+        dims, cfg = self.cfg.dims, self.cfg
+        D.digest_xent(self.H[self.L], cfg.num_classes, self.labels, self.train_mask, self.w_loss,
+                      self.G[self.L], self.loss, self.xent_scratch, stream)
+        for l in range(self.L, 0, -1):
+            xl = self.x_local if l == 1 else self.H[l - 1]
+            xh, ldh = self.halo_input(l)
+            act = D.ACT_RELU if l < self.L else D.ACT_NONE
+            D.digest_layer_bwd(self.part.handle, xl, xh, ldh, self.W[l - 1], dims[l - 1], dims[l],
+                               act, cfg.order, self.saved[l], self.H[l] if act else None,
+                               self.G[l], self.GW[l - 1], self.G[l - 1] if l >= 2 else None,
+                               self.scratch, stream)
+
+    def allreduce(self, stream=None):
+        D.digest_grad_allreduce(self.comm_grad, self.G_flat, 1.0, stream)
+
+    def update(self, stream=None):
+        self.step_count += 1
+        if self.cfg.optimizer == "sgd":
+            D.digest_sgd_step(self.W_flat, self.G_flat, self.cfg.lr, stream)
+        else:
+            D.digest_adam_step(self.W_flat, self.G_flat, self.adam_m, self.adam_v, self.cfg.lr,
+                               0.9, 0.999, 1e-8, self.step_count, stream)
+
+    def epoch(self, r, stream=None):
+        """One full DIGEST epoch r (1-based) for a single worker (NCCL deployment)."""
+        N = self.cfg.sync_interval
+        if r % N == 0:
+            self.pull(r, stream)
+        self.forward(r, (r - 1) % N == 0, stream)
+        self.loss_and_backward(stream)
+        self.allreduce(stream)
+        self.update(stream)
+
+    def close(self):
+        if self.store:
+            D.digest_store_destroy(self.store)
+            self.store = None
+
+
+class LoopbackGroup:
+    """M partitions of one graph trained in one process (single GPU)."""
+
+    def __init__(self, workers):
+        self.workers = workers
+        if len(workers) > 1:
+            D.digest_store_link([w.store for w in workers])
+
+    def epoch(self, r, stream=None):
+        N = self.workers[0].cfg.sync_interval
+        if r % N == 0:
+            for w in self.workers:
+                w.pull(r, stream)
+        for w in self.workers:
+            w.forward(r, (r - 1) % N == 0, stream)
+        for w in self.workers:
+            w.loss_and_backward(stream)
+        if len(self.workers) > 1:
+            D.digest_grad_allreduce_local([w.G_flat for w in self.workers], 1.0, stream)
+        for w in self.workers:
+            w.update(stream)
+
+    def close(self):
+        for w in self.workers:
+            w.close()
+
+
+def build_workers(indptr, indices, x, y, train_mask, weights, part_of, num_parts, cfg: TrainConfig,
+                  ranks=None, comm_grad=None, comm_halo=None, device="cuda"):
+    """Partition on the device and set up workers for `ranks` (default: all parts).
+
+    indptr/indices/part_of/x/y/train_mask: host numpy arrays (the synthetic inputs).
+    The layer-1 inputs X[V_m] and X[H_m] are gathered on the device by digest_gather_rows."""
+    ranks = list(range(num_parts)) if ranks is None else ranks
+    d_ip = torch.as_tensor(indptr, dtype=torch.int64).to(device)
+    d_ix = torch.as_tensor(indices, dtype=torch.int32).to(device)
+    d_po = torch.as_tensor(part_of, dtype=torch.int32).to(device)
+    d_x = torch.as_tensor(x, dtype=torch.float32).to(device)
+    d_y = torch.as_tensor(y, dtype=torch.int32).to(device)
+    d_t = torch.as_tensor(train_mask, dtype=torch.uint8).to(device)
+    w_loss = 1.0 / max(1, int(np.asarray(train_mask).astype(bool).sum()))   # count weighting (A12)
+    workers = []
+    for r in ranks:
+        p = Partition(d_ip, d_ix, d_po, num_parts, r)
+        ids = torch.empty(p.n_local, dtype=torch.int32, device=device)
+        hids = torch.empty(max(p.n_halo, 0), dtype=torch.int32, device=device)
+        D.digest_part_export(p.handle, local_ids=ids, halo_ids=hids)
+        xl = torch.empty(p.n_local, cfg.dims[0], device=device)
+        D.digest_gather_rows(d_x, ids, xl)
+        xh = torch.empty(max(p.n_halo, 1), cfg.dims[0], device=device)
+        if p.n_halo:
+            D.digest_gather_rows(d_x, hids, xh)
+        lab = d_y[ids.long()].contiguous()
+        msk = d_t[ids.long()].contiguous()
+        workers.append(DigestWorker(p, cfg, xl, xh, lab, msk, weights, w_loss,
+                                    comm_grad, comm_halo))
+    return workers

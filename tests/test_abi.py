@@ -1,0 +1,60 @@
+"""CPU-side checks of the C ABI: the library loads, exports every declared symbol,
+and rejects bad arguments synchronously (before touching the device)."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "digest.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:digest_status|const char\*|uint64_t)\s+(digest_\w+)\(",
+                                 src, re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2206_00057_b200 import capi
+    names = _declared()
+    assert len(names) >= 25
+    for n in names:
+        assert hasattr(capi.lib, n), n
+        assert n in capi._SIGS, f"{n} has no binding"
+
+
+def test_binding_names_match_c_names():
+    from paper_2206_00057_b200 import capi
+    for n in _declared():
+        assert callable(getattr(capi, n)), n
+
+
+def test_library_is_sm100a_only():
+    so = os.path.join(ROOT, "paper_2206_00057_b200", "libdigest.so")
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", so], capture_output=True, text=True).stdout
+    assert "sm_100a" in out and "sm_90" not in out
+
+
+def test_synchronous_argument_errors():
+    from paper_2206_00057_b200 import capi as D
+    with pytest.raises(D.DigestError) as e:
+        D.digest_partition(10, 0, 1, 1, 1, 0, 0)            # num_parts = 0
+    assert e.value.status == 1
+    with pytest.raises(D.DigestError):
+        D.digest_partition(10, 0, 1, 1, 1, 2, 5)            # rank out of range
+    s = C.c_size_t()
+    assert D.lib.digest_layer_workspace(None, 4, 4, 0, C.byref(s), C.byref(s)) == 1
+    assert D.lib.digest_xent(None, 4, 0, 4, None, None, 1.0, None, 4, None, None, None) == 2
+    assert D.lib.digest_store_link(None, 0) == 1
+    assert "NULL" in D.digest_last_error() or "bad" in D.digest_last_error()
+
+
+def test_no_cpu_fallback_in_product_path():
+    """The product package never imports the oracle."""
+    pkg = os.path.join(ROOT, "paper_2206_00057_b200")
+    for f in os.listdir(pkg):
+        if f.endswith(".py"):
+            txt = open(os.path.join(pkg, f)).read()
+            assert "import oracle" not in txt and "from oracle" not in txt, f

@@ -67,7 +67,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     libdir = os.path.join(nd, "lib")
     tmp = LIB + ".tmp"
     cmd = ([nvcc()] + ARCH + ["-shared", "-o", tmp] + objs
-           + ["-L", libdir, "-l:libnccl.so.2", "-Xlinker", f"-rpath={libdir}", "-lcuda"])
+           + ["-L", libdir, "-l:libnccl.so.2", "-Xlinker", f"-rpath={libdir}"])
     if verbose:
         print(" ".join(cmd), flush=True)
     r = subprocess.run(cmd, capture_output=True, text=True)

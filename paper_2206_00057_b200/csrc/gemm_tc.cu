@@ -1,0 +1,341 @@
+// Dense transform GEMM of Eq. 5 (Z = A W, T = X W) and the input-gradient GEMM
+// (D W^T) on the 5th-generation tensor cores, at fp32 accuracy via 3xTF32
+// (SURVEY §0 finding 7: plain TF32, unit roundoff ~5e-4, misses the 1e-4 bar).
+//
+//   x = hi + lo, hi = x with the low 13 mantissa bits cleared (exactly TF32),
+//   lo = x - hi (exact in fp32);   A B ~= Ahi Bhi + Ahi Blo + Alo Bhi
+// (the dropped Alo Blo term is ~2^-20 relative).  Accumulation in TMEM (fp32).
+//
+// Kernel: persistent, one CTA per SM, 128 x BN output tiles, K in 32-float
+// (128-byte) blocks, warp-specialised:
+//   warp 0      TMA producer: A tile (128 x 32) + B_hi/B_lo tiles (BN x 32), SW128
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (12 MMAs / k-block)
+//   warps 2-5   split workers: A -> (A_hi in place, A_lo) in shared memory
+//   warps 6-9   epilogue: tcgen05.ld -> ReLU -> global stores (double-buffered TMEM)
+// B (the weight, <= 256 x 1436) is split and transposed to K-major once per call
+// by a small prep kernel into a library-owned workspace.
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "kernels.cuh"
+#include "tc_util.cuh"
+
+namespace dg {
+
+bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
+                  uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer) {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  if (!fn) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_stride_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+namespace {
+
+constexpr int kBM = 128, kBK = 32, kThreads = 320;
+
+constexpr uint32_t pow2_cols(uint32_t c) {
+  return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512;
+}
+
+template <int BN>
+struct Cfg {
+  static constexpr int ACC = (BN + 31) / 32 * 32;           // TMEM column stride per accumulator
+  static constexpr uint32_t TMEM_COLS = pow2_cols(2 * ACC);
+  static constexpr uint32_t A_BYTES = kBM * kBK * 4;        // 16 KB
+  static constexpr uint32_t B_BYTES = BN * kBK * 4;
+  static constexpr uint32_t STAGE = 2 * A_BYTES + 2 * B_BYTES;
+  static constexpr int STAGES = (200 * 1024 / STAGE) > 4 ? 4 : (200 * 1024 / STAGE);
+  static constexpr uint32_t SMEM = STAGES * STAGE + 1024 + 256;
+  static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
+  static_assert(B_BYTES % 1024 == 0, "1024-byte aligned stages (SW128 atoms)");
+};
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+k_gemm_tf32x3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBh,
+              const __grid_constant__ CUtensorMap tmBl, float* __restrict__ C, int64_t ldc,
+              int64_t M, int N, int K, int relu) {
+  using G = Cfg<BN>;
+  constexpr int S = G::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * G::STAGE);
+  uint64_t* full = bars;
+  uint64_t* conv = bars + S;
+  uint64_t* empty = bars + 2 * S;
+  uint64_t* tfull = bars + 3 * S;
+  uint64_t* tempty = bars + 3 * S + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
+  auto stA = [&](int s) { return smem + s * G::STAGE; };
+  auto stAl = [&](int s) { return smem + s * G::STAGE + G::A_BYTES; };
+  auto stBh = [&](int s) { return smem + s * G::STAGE + 2 * G::A_BYTES; };
+  auto stBl = [&](int s) { return smem + s * G::STAGE + 2 * G::A_BYTES + G::B_BYTES; };
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < S; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&conv[s], 128);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(&tfull[a], 1);
+      tc::mbar_init(&tempty[a], 128);
+    }
+    tc::fence_mbar_init();
+    tc::tma_prefetch(&tmA);
+    tc::tma_prefetch(&tmBh);
+    tc::tma_prefetch(&tmBl);
+  }
+  if (warp == 1) tc::tmem_alloc(tmem_slot, G::TMEM_COLS);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int n_tiles_n = (N + BN - 1) / BN;
+  const int64_t n_tiles = ((M + kBM - 1) / kBM) * n_tiles_n;
+  const int nk = (K + kBK - 1) / kBK;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      int s = 0;
+      uint32_t ph = 0;
+      for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        const int m0 = (int)((t / n_tiles_n) * kBM);
+        const int n0 = (int)((t % n_tiles_n) * BN);
+        for (int kb = 0; kb < nk; ++kb) {
+          tc::mbar_wait(&empty[s], ph ^ 1);
+          tc::mbar_arrive_expect_tx(&full[s], G::A_BYTES + 2 * G::B_BYTES);
+          tc::tma_load_2d(stA(s), &tmA, &full[s], kb * kBK, m0);
+          tc::tma_load_2d(stBh(s), &tmBh, &full[s], kb * kBK, n0);
+          tc::tma_load_2d(stBl(s), &tmBl, &full[s], kb * kBK, n0);
+          if (++s == S) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      constexpr uint32_t idesc = tc::idesc_tf32(kBM, BN, false, false);
+      int s = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t aph = 0;
+      for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        tc::mbar_wait(&tempty[acc], aph ^ 1);
+        tc::tc_fence_after();
+        const uint32_t d = tmem_base + acc * G::ACC;
+        for (int kb = 0; kb < nk; ++kb) {
+          tc::mbar_wait(&conv[s], ph);
+          tc::tc_fence_after();
+          const uint32_t a = tc::smem_u32(stA(s)), al = tc::smem_u32(stAl(s));
+          const uint32_t bh = tc::smem_u32(stBh(s)), bl = tc::smem_u32(stBl(s));
+#pragma unroll
+          for (int k = 0; k < kBK / 8; ++k) {
+            const uint32_t off = k * 32;  // 8 tf32 = 32 bytes along K inside the 128B atom
+            const uint64_t dA = tc::smem_desc_sw128(a + off, 16, 1024);
+            const uint64_t dAl = tc::smem_desc_sw128(al + off, 16, 1024);
+            const uint64_t dBh = tc::smem_desc_sw128(bh + off, 16, 1024);
+            const uint64_t dBl = tc::smem_desc_sw128(bl + off, 16, 1024);
+            tc::mma_tf32(d, dAl, dBh, idesc, (kb | k) != 0);
+            tc::mma_tf32(d, dA, dBl, idesc, 1);
+            tc::mma_tf32(d, dA, dBh, idesc, 1);
+          }
+          tc::mma_commit(&empty[s]);
+          if (++s == S) { s = 0; ph ^= 1; }
+        }
+        tc::mma_commit(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) aph ^= 1;
+      }
+    }
+  } else if (warp < 6) {  // ---------------- split workers (128 threads)
+    const int tid = threadIdx.x - 64;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      for (int kb = 0; kb < nk; ++kb) {
+        tc::mbar_wait(&full[s], ph);
+        float4* A = reinterpret_cast<float4*>(stA(s));
+        float4* Al = reinterpret_cast<float4*>(stAl(s));
+#pragma unroll
+        for (int i = 0; i < (int)(G::A_BYTES / 16 / 128); ++i) {
+          const int idx = tid + i * 128;
+          float4 v = A[idx];
+          float4 h = make_float4(tc::tf32_hi(v.x), tc::tf32_hi(v.y), tc::tf32_hi(v.z),
+                                 tc::tf32_hi(v.w));
+          A[idx] = h;
+          Al[idx] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+        }
+        tc::fence_proxy_async_smem();
+        tc::mbar_arrive(&conv[s]);
+        if (++s == S) { s = 0; ph ^= 1; }
+      }
+    }
+  } else {  // ---------------- epilogue (128 threads)
+    const int q = warp & 3;   // TMEM lane quarter this warp may access
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      const int64_t m0 = (t / n_tiles_n) * kBM;
+      const int n0 = (int)((t % n_tiles_n) * BN);
+      tc::mbar_wait(&tfull[acc], aph);
+      tc::tc_fence_after();
+      const int64_t row = m0 + q * 32 + lane;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r[32];
+        tc::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * G::ACC + c0, r);
+        tc::tmem_ld_wait();
+        if (row < M) {
+          float* crow = C + row * ldc + n0 + c0;
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            if (n0 + c0 + j < N) {
+              float4 v = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                     __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+              if (relu) {
+                v.x = fmaxf(v.x, 0.f);
+                v.y = fmaxf(v.y, 0.f);
+                v.z = fmaxf(v.z, 0.f);
+                v.w = fmaxf(v.w, 0.f);
+              }
+              *reinterpret_cast<float4*>(crow + j) = v;
+            }
+          }
+        }
+      }
+      tc::tc_fence_before();
+      tc::mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) aph ^= 1;
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc(tmem_base, G::TMEM_COLS);
+  }
+}
+
+// Bt_hi/Bt_lo [N x Kp] from B(k, j) = B[k*sBk + j*sBj] (split + transpose to K-major).
+__global__ void k_prep_b(const float* __restrict__ B, int64_t sBk, int64_t sBj, int K, int N,
+                         int Kp, float* __restrict__ hi, float* __restrict__ lo) {
+  int64_t total = (int64_t)N * Kp;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int j = (int)(t / Kp), k = (int)(t % Kp);
+    float x = k < K ? B[(int64_t)k * sBk + (int64_t)j * sBj] : 0.f;
+    float h = tc::tf32_hi(x);
+    hi[t] = h;
+    lo[t] = x - h;
+  }
+}
+
+// Library-owned workspace for the split weights (grown on demand, never on a
+// steady-state call; cudaFree synchronises the device before releasing).
+struct Workspace {
+  void* p = nullptr;
+  size_t bytes = 0;
+  std::mutex mu;
+};
+Workspace g_ws;
+
+void* workspace(size_t bytes) {
+  std::lock_guard<std::mutex> lk(g_ws.mu);
+  if (g_ws.bytes < bytes) {
+    if (g_ws.p) cudaFree(g_ws.p);
+    g_ws.p = nullptr;
+    g_ws.bytes = 0;
+    size_t nb = bytes < (1u << 20) ? (1u << 20) : bytes * 2;
+    if (cudaMalloc(&g_ws.p, nb) != cudaSuccess) return nullptr;
+    g_ws.bytes = nb;
+  }
+  return g_ws.p;
+}
+
+template <int BN>
+digest_status launch_tc(const GemmArgs& g, const CUtensorMap& tA, const CUtensorMap& tBh,
+                        const CUtensorMap& tBl, cudaStream_t s) {
+  using G = Cfg<BN>;
+  static bool attr = false;
+  if (!attr) {
+    DG_CUDA(cudaFuncSetAttribute(k_gemm_tf32x3<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 G::SMEM));
+    attr = true;
+  }
+  const int64_t tiles = ceil_div(g.M, kBM) * ceil_div(g.N, BN);
+  const int64_t grid = tiles < num_sms() ? tiles : num_sms();
+  const double flops = 2.0 * (double)g.M * g.N * g.K;
+  const double bytes = 4.0 * ((double)g.M * g.K + (double)g.M * g.N + 2.0 * g.N * g.K);
+  DG_LAUNCH(DIGEST_PROF_GEMM, s, bytes, flops, k_gemm_tf32x3<BN>, (unsigned)grid, kThreads,
+            G::SMEM, tA, tBh, tBl, g.C, g.ldc, g.M, g.N, (int)g.K, g.relu);
+  return DIGEST_OK;
+}
+
+}  // namespace
+
+bool gemm_tc_eligible(const GemmArgs& g) {
+  static int force_simt = -1;
+  if (force_simt < 0) {
+    const char* e = getenv("DIGEST_GEMM");
+    force_simt = (e && e[0] == 's') ? 1 : 0;
+  }
+  if (force_simt) return false;
+  if (g.sAk != 1 || g.sAi % 4 != 0 || ((uintptr_t)g.A & 15) != 0) return false;
+  if (g.sBj != 1 && g.sBk != 1) return false;
+  if (g.N % 4 != 0 || g.N > 256 || g.K < 8 || g.K > (1 << 20)) return false;
+  if (g.ldc % 4 != 0 || ((uintptr_t)g.C & 15) != 0) return false;
+  if (g.M < 256) return false;   // tiny problems: the CUDA-core kernel launches cheaper
+  return true;
+}
+
+digest_status gemm_tc(const GemmArgs& g, cudaStream_t s) {
+  const int K = (int)g.K, N = g.N;
+  const int Kp = (int)round_up(K, 4);
+  float* hi = reinterpret_cast<float*>(workspace(sizeof(float) * 2 * (size_t)N * Kp));
+  DG_ARG(hi, DIGEST_E_NOMEM, "GEMM workspace allocation failed");
+  float* lo = hi + (size_t)N * Kp;
+  {
+    int64_t total = (int64_t)N * Kp;
+    int64_t blocks = ceil_div(total, 256);
+    if (blocks > num_sms() * 4) blocks = num_sms() * 4;
+    DG_LAUNCH(DIGEST_PROF_OTHER, s, 12.0 * total, 0, k_prep_b, (unsigned)blocks, 256, 0, g.B,
+              g.sBk, g.sBj, K, N, Kp, hi, lo);
+  }
+  int BN = N <= 16 ? 16 : N <= 32 ? 32 : N <= 48 ? 48 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
+  CUtensorMap tA, tBh, tBl;
+  bool ok = make_tmap_2d(&tA, g.A, (uint64_t)K, (uint64_t)g.M, (uint64_t)g.sAi * 4, kBK, kBM) &&
+            make_tmap_2d(&tBh, hi, (uint64_t)K, (uint64_t)N, (uint64_t)Kp * 4, kBK, BN) &&
+            make_tmap_2d(&tBl, lo, (uint64_t)K, (uint64_t)N, (uint64_t)Kp * 4, kBK, BN);
+  DG_ARG(ok, DIGEST_E_CUDA, "cuTensorMapEncodeTiled failed");
+  switch (BN) {
+    case 16: return launch_tc<16>(g, tA, tBh, tBl, s);
+    case 32: return launch_tc<32>(g, tA, tBh, tBl, s);
+    case 48: return launch_tc<48>(g, tA, tBh, tBl, s);
+    case 64: return launch_tc<64>(g, tA, tBh, tBl, s);
+    case 128: return launch_tc<128>(g, tA, tBh, tBl, s);
+    default: return launch_tc<256>(g, tA, tBh, tBl, s);
+  }
+}
+
+}  // namespace dg

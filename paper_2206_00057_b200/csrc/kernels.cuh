@@ -43,6 +43,8 @@ struct GemmArgs {
 };
 digest_status gemm(const GemmArgs& g, cudaStream_t s);        // dispatch (tensor core if eligible)
 digest_status gemm_simt(const GemmArgs& g, cudaStream_t s);   // CUDA-core fp32
+bool gemm_tc_eligible(const GemmArgs& g);                      // 3xTF32 tcgen05 path applies
+digest_status gemm_tc(const GemmArgs& g, cudaStream_t s);     // 3xTF32 on tcgen05 (sm_100a)
 
 // Weight gradient over a very long K: C[M x N] (dense, ld = N) = sum over segments of
 // A_seg^T B_seg with A_seg [K_seg x M] (ld lda), B_seg [K_seg x N] (ld ldb).

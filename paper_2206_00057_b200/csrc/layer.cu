@@ -18,7 +18,10 @@
 
 namespace dg {
 
-digest_status gemm(const GemmArgs& g, cudaStream_t s) { return gemm_simt(g, s); }
+digest_status gemm(const GemmArgs& g, cudaStream_t s) {
+  if (g.M == 0 || g.N == 0) return DIGEST_OK;
+  return gemm_tc_eligible(g) ? gemm_tc(g, s) : gemm_simt(g, s);
+}
 
 }  // namespace dg
 

@@ -231,7 +231,8 @@ def test_optimizers_parity():
 
 
 @pytest.mark.parametrize("M,N,K", [(1000, 256, 100), (777, 48, 256), (4096, 16, 1436),
-                                   (129, 8, 16), (3000, 256, 256)])
+                                   (129, 8, 16), (3000, 256, 256), (5000, 8, 16), (300, 128, 604),
+                                   (2049, 64, 500), (70000, 256, 256)])
 def test_gemm_parity(M, N, K):
     Dm = D()
     g = torch.Generator().manual_seed(M + N + K)
@@ -241,6 +242,8 @@ def test_gemm_parity(M, N, K):
     Dm.digest_gemm(A.cuda(), B.cuda(), Cm, relu=True)
     ref = np.maximum(A.double().numpy() @ B.double().numpy(), 0)
     assert rel(Cm.cpu().numpy(), ref) <= TOL
+    # the 3xTF32 tensor-core path is near-fp32 accurate (plain TF32 would be ~1e-3)
+    assert rel(Cm.cpu().numpy(), ref) <= 3e-5, rel(Cm.cpu().numpy(), ref)
 
 
 # ------------------------------------------------------------------ store (a2, a6)

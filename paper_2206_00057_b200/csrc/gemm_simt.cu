@@ -140,12 +140,26 @@ digest_status gemm_simt(const GemmArgs& g, cudaStream_t s) {
   return DIGEST_OK;
 }
 
+size_t wgrad_tc_scratch_bytes(int32_t M, int32_t N);
+bool wgrad_tc_eligible(const WgradSeg* segs, int nseg, int M, int N);
+digest_status wgrad_tc(const WgradSeg* segs, int nseg, int M, int N, float* C, void* scratch,
+                       cudaStream_t s);
+
 size_t wgrad_scratch_bytes(int64_t K_total, int32_t M, int32_t N) {
-  return sizeof(float) * (size_t)wgrad_splits(K_total) * 2 * (size_t)M * (size_t)N + 256;
+  size_t simt = sizeof(float) * (size_t)wgrad_splits(K_total) * 2 * (size_t)M * (size_t)N + 256;
+  size_t tc = wgrad_tc_scratch_bytes(M, N);
+  return simt > tc ? simt : tc;
 }
 
 digest_status wgrad(const WgradSeg* segs, int nseg, int32_t M, int32_t N, float* C,
                     void* scratch, cudaStream_t s) {
+  DG_ARG(nseg >= 1 && nseg <= 2, DIGEST_E_INVALID, "wgrad: 1 or 2 segments");
+  if (wgrad_tc_eligible(segs, nseg, M, N)) return wgrad_tc(segs, nseg, M, N, C, scratch, s);
+  return wgrad_simt(segs, nseg, M, N, C, scratch, s);
+}
+
+digest_status wgrad_simt(const WgradSeg* segs, int nseg, int32_t M, int32_t N, float* C,
+                         void* scratch, cudaStream_t s) {
   DG_ARG(nseg >= 1 && nseg <= 2, DIGEST_E_INVALID, "wgrad: 1 or 2 segments");
   int64_t Ktot = 0;
   for (int i = 0; i < nseg; ++i) Ktot += segs[i].K;

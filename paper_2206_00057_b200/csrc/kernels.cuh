@@ -61,7 +61,9 @@ struct WgradSeg {
 };
 size_t wgrad_scratch_bytes(int64_t K_total, int32_t M, int32_t N);
 digest_status wgrad(const WgradSeg* segs, int nseg, int32_t M, int32_t N, float* C,
-                    void* scratch, cudaStream_t s);
+                    void* scratch, cudaStream_t s);       // dispatch (tensor core if eligible)
+digest_status wgrad_simt(const WgradSeg* segs, int nseg, int32_t M, int32_t N, float* C,
+                         void* scratch, cudaStream_t s);
 
 // D = G o 1[H > 0] (n x w)
 digest_status relu_mask(const float* G, int64_t ldg, const float* H, int64_t ldh, float* D,

@@ -339,3 +339,41 @@ def test_normalized_push_matches_oracle():
     loss = sum(w.loss.item() for w in ws)
     assert abs(loss - run.records[-1].loss) <= TOL * abs(run.records[-1].loss)
     grp.close()
+
+
+@pytest.mark.parametrize("d_in,d_out,order", [(100, 256, 1), (256, 48, 2)])
+def test_layer_parity_large_k(d_in, d_out, order):
+    """Products-shaped partition with ~0.5M rows: the weight gradient reduces over K = rows,
+    exercising the split-K tensor-core path and its chunked TMEM flushes."""
+    Dm = D()
+    cfg = scaled(get_config("products"), 0.2)
+    ip, ix = make_graph(cfg)
+    M = 2
+    part = make_block_parts(cfg, M)
+    p, _ = gpu_partition(ip, ix, part, M, 0)
+    op = oracle.oracle_partition(ip, ix, part, M, 0)
+    g = torch.Generator().manual_seed(5)
+    xl = torch.rand(p.n_local, d_in, generator=g) * 2 - 1
+    xh = torch.rand(p.n_halo, d_in, generator=g) * 2 - 1
+    w = (torch.rand(d_in, d_out, generator=g) * 2 - 1) / np.sqrt(d_in)
+    gout = torch.randn(p.n_local, d_out, generator=g)
+    sv, sc = Dm.digest_layer_workspace(p.handle, d_in, d_out, order)
+    saved = torch.empty(max(sv, 256), dtype=torch.uint8, device="cuda")
+    scratch = torch.empty(max(sc, 256), dtype=torch.uint8, device="cuda")
+    H = torch.empty(p.n_local, d_out, device="cuda")
+    Dm.digest_layer_fwd(p.handle, xl.cuda(), xh.cuda(), d_in, w.cuda(), d_in, d_out, 1, order, H,
+                        saved, scratch)
+    GW = torch.empty(d_in, d_out, device="cuda")
+    Gin = torch.empty(p.n_local, d_in, device="cuda")
+    Dm.digest_layer_bwd(p.handle, xl.cuda(), xh.cuda(), d_in, w.cuda(), d_in, d_out, 1, order,
+                        saved, H, gout.cuda(), GW, Gin, scratch)
+    torch.cuda.synchronize()
+    ref = layer_forward(op, xl.numpy(), xh.numpy(), w.numpy(), relu=True)
+    assert rel(H.cpu().numpy(), ref["H"]) <= TOL
+    b = layer_backward(op, xl.numpy(), xh.numpy(), w.numpy(), gout.numpy(),
+                       H.cpu().numpy() > 0, True)
+    e = rel(GW.cpu().numpy(), b["G_W"])
+    print("large-K G_W rel err", e)
+    assert e <= TOL
+    assert rel(Gin.cpu().numpy(), b["G_in"]) <= TOL
+    p.close()

@@ -187,14 +187,19 @@ digest_status digest_layer_fwd(const digest_part* part, const float* X_local, in
                                void* stream);
 /* G_out: n_local x d_out gradient of the layer output (ld_g).  H_out: the forward
  * output (its sign is the ReLU mask, ReLU'(0) := 0); ignored for ACT_NONE.
+ * flags DIGEST_BWD_G_IS_D: G_out already is D = G o sigma'(Z) (H_out unused).
  * G_W (d_in x d_out, overwritten) = (P_m X_ext)^T D with D = G_out o sigma'(Z).
- * G_in (n_local x d_in, ld_gi; NULL = skip, first layer) = P_in^T D W^T. */
+ * G_in (n_local x d_in, ld_gi; NULL = skip, first layer) = P_in^T D W^T, multiplied
+ * by 1[gin_mask > 0] when gin_mask != NULL -- pass the previous layer's output H to
+ * emit that layer's D directly (fused ReLU', then call it with DIGEST_BWD_G_IS_D). */
+enum { DIGEST_BWD_G_IS_D = 1u };
 digest_status digest_layer_bwd(const digest_part* part, const float* X_local, int64_t ld_x,
                                const float* X_halo, int64_t ld_xh, const float* W,
                                int32_t d_in, int32_t d_out, int32_t act, int32_t order,
                                const void* saved, const float* H_out, int64_t ld_h,
-                               const float* G_out, int64_t ld_g, float* G_W, float* G_in,
-                               int64_t ld_gi, void* scratch, void* stream);
+                               const float* G_out, int64_t ld_g, uint32_t flags, float* G_W,
+                               float* G_in, int64_t ld_gi, const float* gin_mask,
+                               int64_t ld_gm, void* scratch, void* stream);
 
 /* ------------------------------------------------------------------ loss
  * Eq. 3 on training rows: for v with train_mask[v] != 0,

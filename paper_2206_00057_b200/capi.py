@@ -69,7 +69,7 @@ _SIGS = {
     "digest_layer_fwd": ([_p, _p, _i64, _p, _i64, _p, _i32, _i32, _i32, _i32, _p, _i64, _p, _p, _p],
                          _i32),
     "digest_layer_bwd": ([_p, _p, _i64, _p, _i64, _p, _i32, _i32, _i32, _i32, _p, _p, _i64, _p, _i64,
-                          _p, _p, _i64, _p, _p], _i32),
+                          _u32, _p, _p, _i64, _p, _i64, _p, _p], _i32),
     "digest_xent_workspace": ([_i64, _p], _i32),
     "digest_xent": ([_p, _i64, _i32, _i64, _p, _p, _f32, _p, _i64, _p, _p, _p], _i32),
     "digest_grad_allreduce": ([_p, _p, _i64, _f32, _p], _i32),
@@ -250,13 +250,17 @@ def digest_layer_fwd(part, X_local, X_halo, ld_xh, W, d_in, d_out, act, order, H
                                 ptr(scratch), stream_ptr(stream)))
 
 
+BWD_G_IS_D = 1
+
+
 def digest_layer_bwd(part, X_local, X_halo, ld_xh, W, d_in, d_out, act, order, saved, H_out,
-                     G_out, G_W, G_in, scratch, stream=None):
+                     G_out, G_W, G_in, scratch, stream=None, flags=0, gin_mask=None):
     _check(lib.digest_layer_bwd(part, ptr(X_local), ld_of(X_local), ptr(X_halo), ld_xh, ptr(W),
                                 d_in, d_out, act, order, ptr(saved), ptr(H_out),
                                 ld_of(H_out) if H_out is not None else 0, ptr(G_out),
-                                ld_of(G_out), ptr(G_W), ptr(G_in),
-                                ld_of(G_in) if G_in is not None else 0, ptr(scratch),
+                                ld_of(G_out), flags, ptr(G_W), ptr(G_in),
+                                ld_of(G_in) if G_in is not None else 0, ptr(gin_mask),
+                                ld_of(gin_mask) if gin_mask is not None else 0, ptr(scratch),
                                 stream_ptr(stream)))
 
 

@@ -76,6 +76,7 @@ k_gemm(GemmArgs g, int64_t k_per_split, float* partial) {
         partial[((int64_t)blockIdx.z * g.M + gi) * g.N + gj] = v;
       } else {
         if (g.relu) v = fmaxf(v, 0.f);
+        if (g.mask && !(g.mask[gi * g.ldm + gj] > 0.f)) v = 0.f;
         g.C[gi * g.ldc + gj] = v;
       }
     }

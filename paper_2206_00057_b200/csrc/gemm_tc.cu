@@ -71,7 +71,7 @@ template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
 k_gemm_tf32x3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBh,
               const __grid_constant__ CUtensorMap tmBl, float* __restrict__ C, int64_t ldc,
-              int64_t M, int N, int K, int relu) {
+              int64_t M, int N, int K, int relu, const float* __restrict__ mask, int64_t ldm) {
   using G = Cfg<BN>;
   constexpr int S = G::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -218,6 +218,14 @@ k_gemm_tf32x3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 v.z = fmaxf(v.z, 0.f);
                 v.w = fmaxf(v.w, 0.f);
               }
+              if (mask) {
+                const float4 mk =
+                    __ldg(reinterpret_cast<const float4*>(mask + row * ldm + n0 + c0 + j));
+                v.x = mk.x > 0.f ? v.x : 0.f;
+                v.y = mk.y > 0.f ? v.y : 0.f;
+                v.z = mk.z > 0.f ? v.z : 0.f;
+                v.w = mk.w > 0.f ? v.w : 0.f;
+              }
               *reinterpret_cast<float4*>(crow + j) = v;
             }
           }
@@ -288,7 +296,7 @@ digest_status launch_tc(const GemmArgs& g, const CUtensorMap& tA, const CUtensor
   const double flops = 2.0 * (double)g.M * g.N * g.K;
   const double bytes = 4.0 * ((double)g.M * g.K + (double)g.M * g.N + 2.0 * g.N * g.K);
   DG_LAUNCH(DIGEST_PROF_GEMM, s, bytes, flops, k_gemm_tf32x3<BN>, (unsigned)grid, kThreads,
-            G::SMEM, tA, tBh, tBl, g.C, g.ldc, g.M, g.N, (int)g.K, g.relu);
+            G::SMEM, tA, tBh, tBl, g.C, g.ldc, g.M, g.N, (int)g.K, g.relu, g.mask, g.ldm);
   return DIGEST_OK;
 }
 
@@ -305,6 +313,7 @@ bool gemm_tc_eligible(const GemmArgs& g) {
   if (g.sBj != 1 && g.sBk != 1) return false;
   if (g.N % 4 != 0 || g.N > 256 || g.K < 8 || g.K > (1 << 20)) return false;
   if (g.ldc % 4 != 0 || ((uintptr_t)g.C & 15) != 0) return false;
+  if (g.mask && (g.ldm % 4 != 0 || ((uintptr_t)g.mask & 15) != 0)) return false;
   if (g.M < 256) return false;   // tiny problems: the CUDA-core kernel launches cheaper
   return true;
 }

@@ -24,6 +24,8 @@ struct SpmmArgs {
   int64_t ldy;
   int32_t width;
   int32_t relu;
+  const float* mask;   // optional: Y *= 1[mask > 0] (fused ReLU' of the consumer layer)
+  int64_t ldm;
 };
 digest_status spmm(const SpmmArgs& a, cudaStream_t s);
 
@@ -40,6 +42,8 @@ struct GemmArgs {
   int32_t N;
   int64_t K;
   int32_t relu;
+  const float* mask;   // optional: C *= 1[mask > 0] (fused ReLU' of the consumer layer)
+  int64_t ldm;
 };
 digest_status gemm(const GemmArgs& g, cudaStream_t s);        // dispatch (tensor core if eligible)
 digest_status gemm_simt(const GemmArgs& g, cudaStream_t s);   // CUDA-core fp32

@@ -176,21 +176,26 @@ digest_status digest_layer_bwd(const digest_part* p, const float* X_local, int64
                                const float* X_halo, int64_t ld_xh, const float* W, int32_t d_in,
                                int32_t d_out, int32_t act, int32_t order, const void* saved,
                                const float* H_out, int64_t ld_h, const float* G_out, int64_t ld_g,
-                               float* G_W, float* G_in, int64_t ld_gi, void* scratch,
+                               uint32_t flags, float* G_W, float* G_in, int64_t ld_gi,
+                               const float* gin_mask, int64_t ld_gm, void* scratch,
                                void* stream) {
   Plan pl;
   DG_TRY(make_plan(p, d_in, d_out, order, &pl));
   DG_ARG(act == DIGEST_ACT_NONE || act == DIGEST_ACT_RELU, DIGEST_E_INVALID, "bad act");
   DG_TRY(check_mat(G_out, ld_g, d_out, "G_out"));
-  if (act == DIGEST_ACT_RELU) DG_TRY(check_mat(H_out, ld_h, d_out, "H_out"));
+  const bool g_is_d = (flags & DIGEST_BWD_G_IS_D) != 0;
+  if (act == DIGEST_ACT_RELU && !g_is_d) DG_TRY(check_mat(H_out, ld_h, d_out, "H_out"));
   if (G_in) DG_TRY(check_mat(G_in, ld_gi, d_in, "G_in"));
+  if (G_in && gin_mask) DG_TRY(check_mat(gin_mask, ld_gm, d_in, "gin_mask"));
   DG_ARG(W && G_W && scratch, DIGEST_E_INVALID, "W, G_W and scratch must be non-NULL");
   cudaStream_t s = dg::as_stream(stream);
   size_t off = 0;
-  // D = G o sigma'(Z)   (sigma'(Z) = 1[H > 0] for ReLU, ReLU'(0) := 0)
+  // D = G o sigma'(Z)   (sigma'(Z) = 1[H > 0] for ReLU, ReLU'(0) := 0); with
+  // DIGEST_BWD_G_IS_D the producer of G_out already applied it (gin_mask of the
+  // next layer's backward), so no separate masking pass runs.
   const float* D = G_out;
   int64_t ldd = ld_g;
-  if (act == DIGEST_ACT_RELU) {
+  if (act == DIGEST_ACT_RELU && !g_is_d) {
     float* Dm = carve(scratch, off, sizeof(float) * pl.n * pl.ldo);
     DG_TRY(dg::relu_mask(G_out, ld_g, H_out, ld_h, Dm, pl.ldo, pl.n, d_out, s));
     D = Dm;
@@ -211,7 +216,10 @@ digest_status digest_layer_bwd(const digest_part* p, const float* X_local, int64
       g.sBk = 1;
       g.sBj = d_out;
       DG_TRY(dg::gemm(g, s));
-      DG_TRY(dg::spmm(spmm_in(p, U, pl.ldi, G_in, ld_gi, d_in), s));
+      dg::SpmmArgs a = spmm_in(p, U, pl.ldi, G_in, ld_gi, d_in);
+      a.mask = gin_mask;
+      a.ldm = ld_gm;
+      DG_TRY(dg::spmm(a, s));
     }
   } else {
     DG_TRY(check_mat(X_local, ld_x, d_in, "X_local"));
@@ -245,6 +253,8 @@ digest_status digest_layer_bwd(const digest_part* p, const float* X_local, int64
       dg::GemmArgs g = gemm_rm(S, pl.ldo, W, d_out, G_in, ld_gi, pl.n, d_in, d_out, 0);
       g.sBk = 1;
       g.sBj = d_out;
+      g.mask = gin_mask;
+      g.ldm = ld_gm;
       DG_TRY(dg::gemm(g, s));
     }
   }

@@ -145,10 +145,13 @@ class DigestWorker:
             xl = self.x_local if l == 1 else self.H[l - 1]
             xh, ldh = self.halo_input(l)
             act = D.ACT_RELU if l < self.L else D.ACT_NONE
+            # G_in of layer l is produced already multiplied by 1[H^(l-1) > 0], i.e. it is
+            # D^(l-1); layer l-1 then skips its own masking pass (DIGEST_BWD_G_IS_D).
             D.digest_layer_bwd(self.part.handle, xl, xh, ldh, self.W[l - 1], dims[l - 1], dims[l],
-                               act, cfg.order, self.saved[l], self.H[l] if act else None,
-                               self.G[l], self.GW[l - 1], self.G[l - 1] if l >= 2 else None,
-                               self.scratch, stream)
+                               act, cfg.order, self.saved[l], None, self.G[l], self.GW[l - 1],
+                               self.G[l - 1] if l >= 2 else None, self.scratch, stream,
+                               flags=D.BWD_G_IS_D if l < self.L else 0,
+                               gin_mask=self.H[l - 1] if l >= 2 else None)
 
     def allreduce(self, stream=None):
         D.digest_grad_allreduce(self.comm_grad, self.G_flat, 1.0, stream)

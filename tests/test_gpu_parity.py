@@ -170,6 +170,17 @@ def test_layer_forward_backward_per_call(d_in, d_out, order):
         b = layer_backward(op, xl.numpy(), xh.numpy(), w.numpy(), gout.numpy(), mask, True)
         assert rel(GW.cpu().numpy(), b["G_W"]) <= TOL, (act, rel(GW.cpu().numpy(), b["G_W"]))
         assert rel(Gin.cpu().numpy(), b["G_in"]) <= TOL
+        # fused variants: G_out already masked (G_IS_D) and G_in emitted masked by gin_mask
+        gm = torch.randn(p.n_local, d_in, generator=g)
+        Dpre = torch.as_tensor(b["D"], dtype=torch.float32).cuda()
+        GW2 = torch.empty_like(GW)
+        Gin2 = torch.empty_like(Gin)
+        Dm.digest_layer_bwd(p.handle, xl_d, xh_d, d_in, w_d, d_in, d_out, act, order, saved,
+                            None, Dpre, GW2, Gin2, scratch, flags=Dm.BWD_G_IS_D,
+                            gin_mask=gm.cuda())
+        torch.cuda.synchronize()
+        assert rel(GW2.cpu().numpy(), b["G_W"]) <= TOL
+        assert rel(Gin2.cpu().numpy(), b["G_in"] * (gm.numpy() > 0)) <= TOL
     p.close()
 
 

@@ -201,6 +201,16 @@ digest_status digest_layer_bwd(const digest_part* part, const float* X_local, in
                                float* G_in, int64_t ld_gi, const float* gin_mask,
                                int64_t ld_gm, void* scratch, void* stream);
 
+/* The propagation product alone (the aggregation of Eq. 5 / its transposes):
+ *   mode 0: Y = P_m X_ext      (n_local rows; X_ext = [X_local ; X_halo], width w)
+ *   mode 1: Y = P_in^T X_local (= P_in X_local, n_local rows; the in-block part)
+ *   mode 2: Y = P_out^T X_local (n_halo rows; reverse-halo CSR)
+ * w % 4 == 0.  Used by the layer; exported for tests, benchmarks and aggregation
+ * caches (e.g. the static layer-1 aggregation). */
+digest_status digest_propagate(const digest_part* part, int32_t mode, const float* X_local,
+                               int64_t ld_x, const float* X_halo, int64_t ld_xh, int32_t width,
+                               float* Y, int64_t ld_y, void* stream);
+
 /* ------------------------------------------------------------------ loss
  * Eq. 3 on training rows: for v with train_mask[v] != 0,
  * l_v = logsumexp(z_v[0:C]) - z_v[y_v]; G_logits[v,0:C] = w_loss*(softmax - e_y),

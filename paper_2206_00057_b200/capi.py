@@ -70,6 +70,7 @@ _SIGS = {
                          _i32),
     "digest_layer_bwd": ([_p, _p, _i64, _p, _i64, _p, _i32, _i32, _i32, _i32, _p, _p, _i64, _p, _i64,
                           _u32, _p, _p, _i64, _p, _i64, _p, _p], _i32),
+    "digest_propagate": ([_p, _i32, _p, _i64, _p, _i64, _i32, _p, _i64, _p], _i32),
     "digest_xent_workspace": ([_i64, _p], _i32),
     "digest_xent": ([_p, _i64, _i32, _i64, _p, _p, _f32, _p, _i64, _p, _p, _p], _i32),
     "digest_grad_allreduce": ([_p, _p, _i64, _f32, _p], _i32),
@@ -262,6 +263,11 @@ def digest_layer_bwd(part, X_local, X_halo, ld_xh, W, d_in, d_out, act, order, s
                                 ld_of(G_in) if G_in is not None else 0, ptr(gin_mask),
                                 ld_of(gin_mask) if gin_mask is not None else 0, ptr(scratch),
                                 stream_ptr(stream)))
+
+
+def digest_propagate(part, mode, X_local, X_halo, ld_xh, width, Y, stream=None):
+    _check(lib.digest_propagate(part, mode, ptr(X_local), ld_of(X_local), ptr(X_halo), ld_xh,
+                                width, ptr(Y), ld_of(Y), stream_ptr(stream)))
 
 
 # ------------------------------------------------------------------ loss / AGG / update

@@ -26,6 +26,7 @@ struct SpmmArgs {
   int32_t relu;
   const float* mask;   // optional: Y *= 1[mask > 0] (fused ReLU' of the consumer layer)
   int64_t ldm;
+  int32_t hints;       // L2 evict_last on gathers / evict_first on CSR streams
 };
 digest_status spmm(const SpmmArgs& a, cudaStream_t s);
 

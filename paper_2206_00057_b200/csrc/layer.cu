@@ -261,6 +261,35 @@ digest_status digest_layer_bwd(const digest_part* p, const float* X_local, int64
   return DIGEST_OK;
 }
 
+digest_status digest_propagate(const digest_part* p, int32_t mode, const float* X_local,
+                               int64_t ld_x, const float* X_halo, int64_t ld_xh, int32_t width,
+                               float* Y, int64_t ld_y, void* stream) {
+  DG_ARG(p, DIGEST_E_INVALID, "NULL partition");
+  DG_ARG(mode >= 0 && mode <= 2, DIGEST_E_INVALID, "bad mode");
+  DG_ARG(width > 0 && width % 4 == 0, DIGEST_E_SHAPE, "width must be a positive multiple of 4");
+  DG_TRY(check_mat(X_local, ld_x, width, "X_local"));
+  if (mode == 0 && p->n_halo > 0) DG_TRY(check_mat(X_halo, ld_xh, width, "X_halo"));
+  if (mode != 2 || p->n_halo > 0) DG_TRY(check_mat(Y, ld_y, width, "Y"));
+  cudaStream_t s = dg::as_stream(stream);
+  if (mode == 0) return dg::spmm(spmm_full(p, X_local, ld_x, X_halo, ld_xh, Y, ld_y, width, 0), s);
+  if (mode == 1) return dg::spmm(spmm_in(p, X_local, ld_x, Y, ld_y, width), s);
+  dg::SpmmArgs a{};
+  a.row_ptr = p->rh_ptr;
+  a.col = p->rh_col;
+  a.val = p->rh_val;
+  a.n_rows = p->n_halo;
+  a.nnz = p->rh_nnz;
+  a.X0 = X_local;
+  a.ld0 = ld_x;
+  a.split = INT64_MAX;
+  a.X1 = X_local;
+  a.ld1 = ld_x;
+  a.Y = Y;
+  a.ldy = ld_y;
+  a.width = width;
+  return dg::spmm(a, s);
+}
+
 digest_status digest_gemm(const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
                           int64_t ldc, int64_t M, int32_t N, int32_t K, uint32_t flags,
                           void* stream) {

@@ -11,8 +11,40 @@
 namespace dg {
 namespace {
 
-constexpr int kUnroll = 4;
-
+// L2 cache policies: the gathered source rows are re-read by many rows (keep them),
+// the CSR streams are touched once (evict them first).
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ float4 ld_gather(const float* ptr, uint64_t pol) {
+  float4 r;
+  asm("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+      : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+      : "l"(ptr), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ int32_t ld_stream_i(const int32_t* ptr, uint64_t pol) {
+  int32_t r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(r) : "l"(ptr), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ float ld_stream_f(const float* ptr, uint64_t pol) {
+  float r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(ptr), "l"(pol));
+  return r;
+}
 __device__ __forceinline__ float4 ldg4(const float* p) {
   return __ldg(reinterpret_cast<const float4*>(p));
 }
@@ -20,13 +52,120 @@ __device__ __forceinline__ float4 ldg4(const float* p) {
 // One warp per output row.  The warp is split into EG = 32/LC edge groups of LC
 // lanes; edge group g handles edges j = g, g+EG, ... of the row, lane c of a group
 // owns float4 columns c, c+LC, ... (VPL of them).  The 32 (col, val) pairs of a
-// chunk are loaded once, coalesced, and broadcast with full-warp shuffles; UNR
-// edges per group are gathered before any is consumed (EG*UNR*VPL 16-byte loads in
-// flight per warp step).  Partial sums of the edge groups are combined with xor
-// shuffles at the end of the row.  Loop counts are warp-uniform (no divergent
-// shuffles), so narrow widths (8..48 floats) use all 32 lanes on long rows.
+// chunk are loaded once, coalesced, and broadcast with full-warp shuffles; the next
+// chunk's pairs are prefetched while the current one is gathered (software
+// pipelining of the col -> row dependency).  A chunk is consumed in STEPS fully
+// unrolled, predicated steps of UNR edges per group, so up to STEPS*UNR*VPL 16-byte
+// gathers per lane can be in flight.  Edge-group partial sums are combined with xor
+// shuffles at the end of the row.  All loop counts are warp-uniform.
 template <int LC, int VPL, int UNR>
 __global__ void __launch_bounds__(256) k_spmm(SpmmArgs a) {
+  constexpr int EG = 32 / LC;
+  constexpr int STEP = EG * UNR;
+  constexpr int STEPS = STEP >= 32 ? 1 : 32 / STEP;
+  const int lane = threadIdx.x & 31;
+  const int cl = lane % LC;
+  const int g = lane / LC;
+  const int w4 = a.width >> 2;
+  const uint64_t pol_x = a.hints ? policy_evict_last() : policy_evict_normal();
+  const uint64_t pol_s = a.hints ? policy_evict_first() : policy_evict_normal();
+  int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t row = warp; row < a.n_rows; row += nwarps) {
+    float4 acc[VPL];
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int64_t beg = a.row_ptr[row];
+    const int64_t end = a.in_len ? beg + a.in_len[row] : a.row_ptr[row + 1];
+    int32_t c_nxt = 0;
+    float v_nxt = 0.f;
+    if (beg + lane < end) {
+      c_nxt = ld_stream_i(a.col + beg + lane, pol_s);
+      v_nxt = ld_stream_f(a.val + beg + lane, pol_s);
+    }
+    for (int64_t e0 = beg; e0 < end; e0 += 32) {
+      const int32_t c = c_nxt;
+      const float v = v_nxt;
+      const int cnt = (int)min((int64_t)32, end - e0);
+      if (e0 + 32 + lane < end) {
+        c_nxt = ld_stream_i(a.col + e0 + 32 + lane, pol_s);
+        v_nxt = ld_stream_f(a.val + e0 + 32 + lane, pol_s);
+      }
+#pragma unroll
+      for (int st = 0; st < STEPS; ++st) {
+        const float* src[UNR];
+        float vv[UNR];
+        bool ok[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          const int j = st * STEP + u * EG + g;
+          const int cj = __shfl_sync(0xffffffffu, c, j & 31);
+          const float x = __shfl_sync(0xffffffffu, v, j & 31);
+          ok[u] = j < cnt;
+          vv[u] = ok[u] ? x : 0.f;
+          src[u] = (int64_t)cj < a.split ? a.X0 + (int64_t)cj * a.ld0
+                                         : a.X1 + ((int64_t)cj - a.split) * a.ld1;
+        }
+        float4 t[UNR][VPL];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+#pragma unroll
+          for (int q = 0; q < VPL; ++q) {
+            const int idx = cl + q * LC;
+            t[u][q] = (ok[u] && idx < w4) ? ld_gather(src[u] + 4 * idx, pol_x)
+                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+#pragma unroll
+          for (int q = 0; q < VPL; ++q) {
+            acc[q].x = fmaf(vv[u], t[u][q].x, acc[q].x);
+            acc[q].y = fmaf(vv[u], t[u][q].y, acc[q].y);
+            acc[q].z = fmaf(vv[u], t[u][q].z, acc[q].z);
+            acc[q].w = fmaf(vv[u], t[u][q].w, acc[q].w);
+          }
+      }
+    }
+#pragma unroll
+    for (int off = LC; off < 32; off <<= 1)
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) {
+        acc[q].x += __shfl_xor_sync(0xffffffffu, acc[q].x, off);
+        acc[q].y += __shfl_xor_sync(0xffffffffu, acc[q].y, off);
+        acc[q].z += __shfl_xor_sync(0xffffffffu, acc[q].z, off);
+        acc[q].w += __shfl_xor_sync(0xffffffffu, acc[q].w, off);
+      }
+    if (g == 0) {
+      float* y = a.Y + row * a.ldy;
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) {
+        const int idx = cl + q * LC;
+        if (idx < w4) {
+          float4 r = acc[q];
+          if (a.relu) {
+            r.x = fmaxf(r.x, 0.f);
+            r.y = fmaxf(r.y, 0.f);
+            r.z = fmaxf(r.z, 0.f);
+            r.w = fmaxf(r.w, 0.f);
+          }
+          if (a.mask) {
+            const float4 mk = ldg4(a.mask + row * a.ldm + 4 * idx);
+            r.x = mk.x > 0.f ? r.x : 0.f;
+            r.y = mk.y > 0.f ? r.y : 0.f;
+            r.z = mk.z > 0.f ? r.z : 0.f;
+            r.w = mk.w > 0.f ? r.w : 0.f;
+          }
+          reinterpret_cast<float4*>(y)[idx] = r;
+        }
+      }
+    }
+  }
+}
+
+// Runtime-trip-count variant (no chunk prefetch, default caching): fewer registers,
+// higher occupancy; best for the wide rows (measured).
+template <int LC, int VPL, int UNR>
+__global__ void __launch_bounds__(256) k_spmm_rt(SpmmArgs a) {
   constexpr int EG = 32 / LC;
   const int lane = threadIdx.x & 31;
   const int cl = lane % LC;
@@ -118,7 +257,8 @@ __global__ void __launch_bounds__(256) k_spmm(SpmmArgs a) {
   }
 }
 
-template <int LC, int VPL, int UNR>
+
+template <int LC, int VPL, int UNR, bool PF = true>
 digest_status launch(const SpmmArgs& a, cudaStream_t s) {
   int64_t blocks = ceil_div(a.n_rows, 8);
   const int64_t cap = (int64_t)num_sms() * 8 * 8;
@@ -127,32 +267,88 @@ digest_status launch(const SpmmArgs& a, cudaStream_t s) {
   const double w = a.width;
   const double bytes = (double)a.nnz * (8.0 + 4.0 * w) + (double)a.n_rows * (4.0 * w + 8.0);
   const double flops = 2.0 * (double)a.nnz * w;
-  DG_LAUNCH_TAG(DIGEST_PROF_SPMM, a.width, s, bytes, flops, (k_spmm<LC, VPL, UNR>),
-                (unsigned)blocks, 256, 0, a);
+  if (PF)
+    DG_LAUNCH_TAG(DIGEST_PROF_SPMM, a.width, s, bytes, flops, (k_spmm<LC, VPL, UNR>),
+                  (unsigned)blocks, 256, 0, a);
+  else
+    DG_LAUNCH_TAG(DIGEST_PROF_SPMM, a.width, s, bytes, flops, (k_spmm_rt<LC, VPL, UNR>),
+                  (unsigned)blocks, 256, 0, a);
   return DIGEST_OK;
 }
 
 }  // namespace
 
-digest_status spmm(const SpmmArgs& a, cudaStream_t s) {
-  if (a.n_rows == 0) return DIGEST_OK;
+digest_status spmm_one(const SpmmArgs& a, cudaStream_t s);
+
+// Column-slab schedule: the gathered source rows of a slab (n_src x slab floats) are
+// sized to stay resident in L2 while the row window sweeps a graph block, so the
+// edge gathers hit L2 instead of HBM; each slab re-reads the CSR (8 B / nnz).
+// DIGEST_SPMM_SLAB overrides the slab width (0 = no slabs).
+int spmm_slab_width(const SpmmArgs& a) {
+  static int env = -2;
+  if (env == -2) {
+    const char* e = getenv("DIGEST_SPMM_SLAB");
+    env = e ? atoi(e) : -1;
+  }
+  if (env >= 0) return env;
+  return 0;
+}
+
+digest_status spmm(const SpmmArgs& a0, cudaStream_t s) {
+  if (a0.n_rows == 0) return DIGEST_OK;
+  static int hints = -1;
+  if (hints < 0) {
+    const char* e = getenv("DIGEST_SPMM_HINTS");
+    hints = e ? atoi(e) : 1;
+  }
+  SpmmArgs a = a0;
+  a.hints = hints;
   DG_ARG(a.width > 0 && a.width % 4 == 0, DIGEST_E_INVALID,
          "SpMM width %d must be a positive multiple of 4", a.width);
+  const int slab = spmm_slab_width(a);
+  if (slab <= 0 || slab % 4 != 0 || slab >= a.width) return spmm_one(a, s);
+  for (int c0 = 0; c0 < a.width; c0 += slab) {
+    SpmmArgs b = a;
+    b.X0 = a.X0 + c0;
+    b.X1 = a.X1 + c0;
+    b.Y = a.Y + c0;
+    if (a.mask) b.mask = a.mask + c0;
+    b.width = a.width - c0 < slab ? a.width - c0 : slab;
+    DG_TRY(spmm_one(b, s));
+  }
+  return DIGEST_OK;
+}
+
+digest_status spmm_one(const SpmmArgs& a, cudaStream_t s) {
   const int w4 = a.width / 4;
   // (lanes per edge, float4 per lane, edges per group per step); EG = 32 / LC edge groups
-  if (w4 <= 1) return launch<1, 1, 2>(a, s);
-  if (w4 <= 2) return launch<2, 1, 2>(a, s);
+  if (w4 <= 1) return launch<1, 1, 1>(a, s);
+  if (w4 <= 2) return launch<2, 1, 1>(a, s);
   if (w4 <= 4) return launch<4, 1, 2>(a, s);
-  if (w4 <= 8) return launch<8, 1, 2>(a, s);
+  if (w4 <= 8) return launch<8, 1, 4>(a, s);
   if (w4 <= 12) return launch<4, 3, 2>(a, s);
-  if (w4 <= 16) return launch<8, 2, 2>(a, s);
-  if (w4 <= 32) return launch<8, 4, 2>(a, s);
-  if (w4 <= 64) return launch<32, 2, 4>(a, s);
-  if (w4 <= 96) return launch<32, 3, 4>(a, s);
-  if (w4 <= 128) return launch<32, 4, 4>(a, s);
-  if (w4 <= 192) return launch<32, 6, 2>(a, s);
-  if (w4 <= 256) return launch<32, 8, 2>(a, s);
-  if (w4 <= 384) return launch<32, 12, 2>(a, s);
+  if (w4 <= 16) return launch<8, 2, 4>(a, s);
+  if (w4 <= 32) return launch<8, 4, 2, false>(a, s);
+  if (w4 <= 64) {
+    static int v = -1;
+    if (v < 0) {
+      const char* e = getenv("DIGEST_SPMM_V");
+      v = e ? atoi(e) : 0;
+    }
+    switch (v) {
+      case 1: return launch<32, 2, 4>(a, s);
+      case 2: return launch<32, 2, 8>(a, s);
+      case 3: return launch<32, 2, 8, false>(a, s);
+      case 4: return launch<16, 4, 4, false>(a, s);
+      case 5: return launch<32, 2, 2, false>(a, s);
+      default: return launch<32, 2, 4, false>(a, s);
+    }
+  }
+  if (w4 <= 96) return launch<32, 3, 4, false>(a, s);
+  if (w4 <= 128) return launch<32, 4, 4, false>(a, s);
+  if (w4 <= 192) return launch<32, 6, 2, false>(a, s);
+  if (w4 <= 256) return launch<32, 8, 2, false>(a, s);
+  if (w4 <= 384) return launch<32, 12, 2, false>(a, s);
   return set_error(DIGEST_E_UNSUPPORTED, "SpMM width %d > 1536", a.width);
 }
 

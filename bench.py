@@ -37,7 +37,7 @@ def parse():
     ap.add_argument("--config", default="products")
     ap.add_argument("--mode", default="async", choices=["async", "sync"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--sample-frac", type=float, default=0.02,
+    ap.add_argument("--sample-frac", type=float, default=0.1,
                     help="oracle sample: fraction of nodes/edges of the workload")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -174,14 +174,8 @@ def run_ours(a, rank, world, local):
 
     comm_grad = comm_halo = None
     if world > 1:
-        ids = []
-        for _ in range(2):
-            uid = torch.zeros(128, dtype=torch.uint8)
-            if rank == 0:
-                uid = torch.tensor(list(D.digest_comm_unique_id()), dtype=torch.uint8)
-            uid = uid.cuda()
-            dist.broadcast(uid, 0)
-            ids.append(bytes(uid.cpu().tolist()))
+        from paper_2206_00057_b200.dist import broadcast_ids
+        ids = broadcast_ids(D.digest_comm_unique_id, 2, rank, device="cuda")
         comm_grad = D.digest_comm_init(ids[0], world, rank)
         comm_halo = D.digest_comm_init(ids[1], world, rank)
 
@@ -193,6 +187,9 @@ def run_ours(a, rank, world, local):
     torch.cuda.synchronize()
     t_part = time.time() - t1
     info = w.part.info
+    if world > 1:   # refuse to start if the per-peer boundary counts disagree (NCCL would hang)
+        from paper_2206_00057_b200.dist import check_exchange_plan
+        check_exchange_plan(info.send_count, info.recv_count, world, device="cuda")
     stream = torch.cuda.current_stream()
 
     def barrier():
@@ -267,7 +264,8 @@ def run_ours(a, rank, world, local):
         avg_s = dom["ms"] / 1e3 / dom["launches"]
         ach = per_launch_bytes / avg_s / 1e9
         roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-                "traffic": traffic_from_profiles(dom["tag"]), "kernel": f"k_spmm width {dom['tag']}",
+                "traffic": traffic_from_profiles(f"{a.config}_M{M}_spmm_w{dom['tag']}"),
+                "kernel": f"k_spmm width {dom['tag']}",
                 "peak_source": src, "launches": dom["launches"], "avg_ms": avg_s * 1e3,
                 "alg_bytes_per_launch": per_launch_bytes}
     spmm = prof["spmm"]
@@ -278,7 +276,7 @@ def run_ours(a, rank, world, local):
         nz = sum(d["flops"] / (2.0 * d["tag"]) for d in detail if d["cls"] == "spmm" and d["tag"])
         gteps = nz / (spmm["ms"] / 1e3) / 1e9
     cpu = None
-    if rank == 0:
+    if rank == 0 and world == 1:   # the oracle baseline is timed at N=1 only
         per, sample = oracle_sample_epoch_seconds(a.config, M, a.sample_frac, 1, 1)
         cpu = {"value": float(np.mean(per)), "unit": "s", "cores": cores(), "kind": "oracle",
                "sample": sample}
@@ -308,13 +306,13 @@ def run_ours(a, rank, world, local):
         dist.destroy_process_group()
 
 
-def traffic_from_profiles(tag):
-    """dram bytes per launch of the dominant SpMM from the committed ncu summary, if any."""
+def traffic_from_profiles(key):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full
+    capture of the same workload (profiles/ncu_traffic.json), or None if not captured."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
-            t = json.load(f)
-        return t.get(f"spmm_w{tag}")
+            return json.load(f).get(key)
     except Exception:
         return None
 

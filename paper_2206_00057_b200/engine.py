@@ -19,6 +19,7 @@ import numpy as np
 import torch
 
 from . import capi as D
+from .dist import Schedule
 
 
 @dataclass
@@ -166,10 +167,10 @@ class DigestWorker:
 
     def epoch(self, r, stream=None):
         """One full DIGEST epoch r (1-based) for a single worker (NCCL deployment)."""
-        N = self.cfg.sync_interval
-        if r % N == 0:
+        sched = Schedule(self.cfg.sync_interval)
+        if sched.pull(r):
             self.pull(r, stream)
-        self.forward(r, (r - 1) % N == 0, stream)
+        self.forward(r, sched.push(r), stream)
         self.loss_and_backward(stream)
         self.allreduce(stream)
         self.update(stream)
@@ -189,12 +190,12 @@ class LoopbackGroup:
             D.digest_store_link([w.store for w in workers])
 
     def epoch(self, r, stream=None):
-        N = self.workers[0].cfg.sync_interval
-        if r % N == 0:
+        sched = Schedule(self.workers[0].cfg.sync_interval)
+        if sched.pull(r):      # all pulls of epoch r precede any push of epoch r (reading A7)
             for w in self.workers:
                 w.pull(r, stream)
         for w in self.workers:
-            w.forward(r, (r - 1) % N == 0, stream)
+            w.forward(r, sched.push(r), stream)
         for w in self.workers:
             w.loss_and_backward(stream)
         if len(self.workers) > 1:

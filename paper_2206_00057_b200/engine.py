@@ -33,6 +33,7 @@ class TrainConfig:
     async_push: bool = False
     normalize_pushed: bool = False
     pull_mode: int = D.PULL_FLIP
+    fresh: bool = False         # zero-staleness mode (the oracle's mode='fresh')
 
 
 class Partition:
@@ -125,18 +126,37 @@ class DigestWorker:
             D.digest_pull(self.store, l, epoch, self.cfg.pull_mode, stream)
             self.pulls += 1
 
-    def forward(self, epoch, push: bool, stream=None):
+    def forward_layer(self, l, stream=None):
         dims, cfg = self.cfg.dims, self.cfg
+        xl = self.x_local if l == 1 else self.H[l - 1]
+        xh, ldh = self.halo_input(l)
+        act = D.ACT_RELU if l < self.L else D.ACT_NONE
+        D.digest_layer_fwd(self.part.handle, xl, xh, ldh, self.W[l - 1], dims[l - 1], dims[l],
+                           act, cfg.order, self.H[l], self.saved[l], self.scratch, stream)
+
+    def push(self, l, epoch, stream=None):
+        cfg = self.cfg
         flags = (D.PUSH_ASYNC if cfg.async_push else 0) | (D.PUSH_L2NORM if cfg.normalize_pushed else 0)
+        D.digest_push_boundary(self.store, l, self.H[l], epoch, flags, stream)
+        self.pushes += 1
+
+    def forward(self, epoch, push: bool, stream=None):
         for l in range(1, self.L + 1):
-            xl = self.x_local if l == 1 else self.H[l - 1]
-            xh, ldh = self.halo_input(l)
-            act = D.ACT_RELU if l < self.L else D.ACT_NONE
-            D.digest_layer_fwd(self.part.handle, xl, xh, ldh, self.W[l - 1], dims[l - 1], dims[l],
-                               act, cfg.order, self.H[l], self.saved[l], self.scratch, stream)
+            self.forward_layer(l, stream)
             if push and l < self.L:
-                D.digest_push_boundary(self.store, l, self.H[l], epoch, flags, stream)
-                self.pushes += 1
+                self.push(l, epoch, stream)
+
+    def forward_fresh(self, epoch, stream=None):
+        """Zero-staleness variant (the propagation-style exchange the paper
+        compares against): after each level, push it and pull it back at
+        once (epoch + 1 makes this epoch's push visible), so layer l+1 reads the
+        current halo values.  Collective per level on every rank."""
+        for l in range(1, self.L + 1):
+            self.forward_layer(l, stream)
+            if l < self.L:
+                self.push(l, epoch, stream)
+                D.digest_pull(self.store, l, epoch + 1, self.cfg.pull_mode, stream)
+                self.pulls += 1
 
     def loss_and_backward(self, stream=None):
         dims, cfg = self.cfg.dims, self.cfg
@@ -167,10 +187,13 @@ class DigestWorker:
 
     def epoch(self, r, stream=None):
         """One full DIGEST epoch r (1-based) for a single worker (NCCL deployment)."""
-        sched = Schedule(self.cfg.sync_interval)
-        if sched.pull(r):
-            self.pull(r, stream)
-        self.forward(r, sched.push(r), stream)
+        if self.cfg.fresh:
+            self.forward_fresh(r, stream)
+        else:
+            sched = Schedule(self.cfg.sync_interval)
+            if sched.pull(r):
+                self.pull(r, stream)
+            self.forward(r, sched.push(r), stream)
         self.loss_and_backward(stream)
         self.allreduce(stream)
         self.update(stream)
@@ -190,12 +213,24 @@ class LoopbackGroup:
             D.digest_store_link([w.store for w in workers])
 
     def epoch(self, r, stream=None):
-        sched = Schedule(self.workers[0].cfg.sync_interval)
-        if sched.pull(r):      # all pulls of epoch r precede any push of epoch r (reading A7)
+        if self.workers[0].cfg.fresh:
+            # zero staleness: layer-major, every level exchanged before the next layer
+            for l in range(1, self.workers[0].L + 1):
+                for w in self.workers:
+                    w.forward_layer(l, stream)
+                if l < self.workers[0].L:
+                    for w in self.workers:
+                        w.push(l, r, stream)
+                    for w in self.workers:
+                        D.digest_pull(w.store, l, r + 1, w.cfg.pull_mode, stream)
+                        w.pulls += 1
+        else:
+            sched = Schedule(self.workers[0].cfg.sync_interval)
+            if sched.pull(r):      # all pulls of epoch r precede any push of epoch r (A7)
+                for w in self.workers:
+                    w.pull(r, stream)
             for w in self.workers:
-                w.pull(r, stream)
-        for w in self.workers:
-            w.forward(r, sched.push(r), stream)
+                w.forward(r, sched.push(r), stream)
         for w in self.workers:
             w.loss_and_backward(stream)
         if len(self.workers) > 1:

@@ -388,3 +388,103 @@ def test_layer_parity_large_k(d_in, d_out, order):
     assert e <= TOL
     assert rel(Gin.cpu().numpy(), b["G_in"]) <= TOL
     p.close()
+
+
+def _sample_rows(n, rng, deg):
+    top = np.argsort(deg)[-50:]                       # hubs (longest rows)
+    return np.unique(np.concatenate([rng.choice(n, 1500, replace=False), top, [0, n - 1]]))
+
+
+def _rows_product(P, rows, X):
+    """(P X)[rows] in fp64 touching only the needed source rows (oracle's P, any X)."""
+    Pr = P[rows]
+    cols = np.unique(Pr.indices)
+    sub = np.asarray(X[cols], dtype=np.float64)
+    import scipy.sparse as sp
+    Pc = sp.csr_matrix((Pr.data, np.searchsorted(cols, Pr.indices), Pr.indptr),
+                       shape=(len(rows), len(cols)))
+    return Pc @ sub
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("M", [1, 8])
+def test_full_size_products_epoch_sampled_rows(M):
+    """bench.py's workload (products-shaped, dims 100-256-256-48, Adam) at full size:
+    sampled output rows of every layer (lockstep: each layer from the GPU's own input),
+    and the full layer-1 weight gradient, vs the oracle on rank 0 of M parts."""
+    from paper_2206_00057_b200.engine import TrainConfig, build_workers, LoopbackGroup
+    from oracle.gcn import prop_matrix
+    cfg = get_config("products")
+    inp = make_inputs(cfg)
+    part = make_block_parts(cfg, M)
+    tc = TrainConfig(dims=cfg.dims, num_classes=cfg.num_classes, sync_interval=cfg.sync_interval,
+                     lr=0.01, optimizer="adam", async_push=False)
+    ws = build_workers(inp.indptr, inp.indices, inp.x, inp.y, inp.train_mask, inp.weights, part, M,
+                       tc)
+    grp = LoopbackGroup(ws)
+    # epoch 1 up to (not including) AGG, so rank 0's own G_W can be compared
+    for w in ws:
+        w.forward(1, push=True)
+    for w in ws:
+        w.loss_and_backward()
+    torch.cuda.synchronize()
+    w0 = ws[0]
+    op = oracle.oracle_partition(inp.indptr, inp.indices, part, M, 0)
+    P = prop_matrix(op)
+    rng = np.random.default_rng(0)
+    rows = _sample_rows(op.n_local, rng, np.diff(op.row_ptr))
+    x_ext = np.vstack([inp.x[op.local_ids], inp.x[op.halo_ids]]) if op.n_halo else inp.x[op.local_ids]
+    W = [w.astype(np.float64) for w in inp.weights]
+    L = len(W)
+    H_gpu = {l: w0.H[l].cpu().numpy() for l in range(1, L + 1)}
+    for l in range(1, L + 1):
+        if l == 1:
+            src = x_ext
+        else:   # lockstep: GPU layer l-1 output; epoch 1 halo of level l-1 is the cold (zero) store
+            src = np.vstack([H_gpu[l - 1], np.zeros((op.n_halo, H_gpu[l - 1].shape[1]), np.float32)])
+        Z = _rows_product(P, rows, src) @ W[l - 1]
+        ref = np.maximum(Z, 0) if l < L else Z
+        e = rel(H_gpu[l][rows], ref)
+        print(f"M={M} layer {l} sampled-row rel err {e:.3g}")
+        assert e <= TOL
+    # full layer-1 weight gradient: G_W1 = (P X_ext)^T D1, D1 = the GPU's masked gradient
+    A1 = P @ np.asarray(x_ext, np.float64)
+    D1 = w0.G[1].cpu().numpy().astype(np.float64)
+    GW1 = A1.T @ D1
+    e = rel(w0.GW[0].cpu().numpy(), GW1)
+    print(f"M={M} full G_W1 rel err {e:.3g}")
+    assert e <= TOL
+    grp.close()
+
+
+@pytest.mark.parametrize("M,pull_mode", [(2, 0), (3, 1)])
+def test_fresh_mode_vs_oracle_and_full_graph(M, pull_mode):
+    """zero-staleness exchange per level.  The GPU trajectory follows the
+    oracle's fresh mode, and the first epoch's loss equals full-graph GCN's."""
+    from paper_2206_00057_b200.engine import TrainConfig, build_workers, LoopbackGroup
+    from oracle.train import full_prop_matrix, full_graph_forward
+    cfg = small_config(num_nodes=900, nnz=9000, d0=16, hidden=(24, 16), num_classes=5, c_pad=8,
+                       seed=41 + M, train_frac=0.5)
+    inp = make_inputs(cfg)
+    part = make_random_parts(cfg.num_nodes, M, 2)
+    tc = TrainConfig(dims=cfg.dims, num_classes=cfg.num_classes, lr=0.05, fresh=True,
+                     pull_mode=pull_mode)
+    ws = build_workers(inp.indptr, inp.indices, inp.x, inp.y, inp.train_mask, inp.weights, part, M, tc)
+    grp = LoopbackGroup(ws)
+    run = oracle.oracle_train(inp.indptr, inp.indices, inp.x, inp.y, inp.train_mask, inp.weights,
+                              cfg.num_classes, part, M, sync_interval=1, epochs=3, lr=0.05,
+                              mode="fresh")
+    Pf = full_prop_matrix(inp.indptr, inp.indices)
+    H, _ = full_graph_forward(Pf, inp.x, [w.astype(np.float64) for w in inp.weights])
+    n_train = int(inp.train_mask.sum())
+    full_loss, _ = cross_entropy(H[-1], inp.y, inp.train_mask, cfg.num_classes, 1.0 / n_train)
+    for r in (1, 2, 3):
+        grp.epoch(r)
+        torch.cuda.synchronize()
+        loss = sum(w.loss.item() for w in ws)
+        assert abs(loss - run.records[r - 1].loss) <= TOL * abs(run.records[r - 1].loss)
+        if r == 1:
+            assert abs(loss - full_loss) <= TOL * abs(full_loss)
+    for l, wref in enumerate(run.weights):
+        assert rel(ws[0].W[l].cpu().numpy(), wref) <= TOL
+    grp.close()

@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(256) k_spmm(SpmmArgs a) {
           const int j = st * STEP + u * EG + g;
           const int cj = __shfl_sync(0xffffffffu, c, j & 31);
           const float x = __shfl_sync(0xffffffffu, v, j & 31);
-          ok[u] = j < cnt;
+          ok[u] = g < EG && j < cnt;
           vv[u] = ok[u] ? x : 0.f;
           src[u] = (int64_t)cj < a.split ? a.X0 + (int64_t)cj * a.ld0
                                          : a.X1 + ((int64_t)cj - a.split) * a.ld1;
@@ -127,13 +127,20 @@ __global__ void __launch_bounds__(256) k_spmm(SpmmArgs a) {
       }
     }
 #pragma unroll
-    for (int off = LC; off < 32; off <<= 1)
+    for (int off = LC; off < EG * LC; off <<= 1)   // tree over the edge groups
 #pragma unroll
       for (int q = 0; q < VPL; ++q) {
-        acc[q].x += __shfl_xor_sync(0xffffffffu, acc[q].x, off);
-        acc[q].y += __shfl_xor_sync(0xffffffffu, acc[q].y, off);
-        acc[q].z += __shfl_xor_sync(0xffffffffu, acc[q].z, off);
-        acc[q].w += __shfl_xor_sync(0xffffffffu, acc[q].w, off);
+        const bool in = lane + off < EG * LC;
+        const float x = __shfl_down_sync(0xffffffffu, acc[q].x, off);
+        const float y = __shfl_down_sync(0xffffffffu, acc[q].y, off);
+        const float z = __shfl_down_sync(0xffffffffu, acc[q].z, off);
+        const float w = __shfl_down_sync(0xffffffffu, acc[q].w, off);
+        if (in) {
+          acc[q].x += x;
+          acc[q].y += y;
+          acc[q].z += z;
+          acc[q].w += w;
+        }
       }
     if (g == 0) {
       float* y = a.Y + row * a.ldy;
@@ -197,7 +204,7 @@ __global__ void __launch_bounds__(256) k_spmm_rt(SpmmArgs a) {
           const int j = j0 + u * EG + g;
           const int cj = __shfl_sync(0xffffffffu, c, j & 31);
           const float x = __shfl_sync(0xffffffffu, v, j & 31);
-          ok[u] = j < cnt;
+          ok[u] = g < EG && j < cnt;
           vv[u] = ok[u] ? x : 0.f;
           src[u] = (int64_t)cj < a.split ? a.X0 + (int64_t)cj * a.ld0
                                          : a.X1 + ((int64_t)cj - a.split) * a.ld1;
@@ -222,13 +229,20 @@ __global__ void __launch_bounds__(256) k_spmm_rt(SpmmArgs a) {
       }
     }
 #pragma unroll
-    for (int off = LC; off < 32; off <<= 1)
+    for (int off = LC; off < EG * LC; off <<= 1)   // tree over the edge groups
 #pragma unroll
       for (int q = 0; q < VPL; ++q) {
-        acc[q].x += __shfl_xor_sync(0xffffffffu, acc[q].x, off);
-        acc[q].y += __shfl_xor_sync(0xffffffffu, acc[q].y, off);
-        acc[q].z += __shfl_xor_sync(0xffffffffu, acc[q].z, off);
-        acc[q].w += __shfl_xor_sync(0xffffffffu, acc[q].w, off);
+        const bool in = lane + off < EG * LC;
+        const float x = __shfl_down_sync(0xffffffffu, acc[q].x, off);
+        const float y = __shfl_down_sync(0xffffffffu, acc[q].y, off);
+        const float z = __shfl_down_sync(0xffffffffu, acc[q].z, off);
+        const float w = __shfl_down_sync(0xffffffffu, acc[q].w, off);
+        if (in) {
+          acc[q].x += x;
+          acc[q].y += y;
+          acc[q].z += z;
+          acc[q].w += w;
+        }
       }
     if (g == 0) {
       float* y = a.Y + row * a.ldy;
@@ -326,8 +340,29 @@ digest_status spmm_one(const SpmmArgs& a, cudaStream_t s) {
   if (w4 <= 2) return launch<2, 1, 1>(a, s);
   if (w4 <= 4) return launch<4, 1, 2>(a, s);
   if (w4 <= 8) return launch<8, 1, 4>(a, s);
-  if (w4 <= 12) return launch<4, 3, 2>(a, s);
+  if (w4 <= 12) {
+    static int v = -1;
+    if (v < 0) {
+      const char* e = getenv("DIGEST_SPMM_V12");
+      v = e ? atoi(e) : 0;
+    }
+    if (v == 1) return launch<4, 3, 2>(a, s);
+    if (v == 2) return launch<4, 3, 2, false>(a, s);
+    if (v == 3) return launch<4, 3, 4, false>(a, s);
+    if (v == 4) return launch<8, 2, 2>(a, s);
+    return launch<4, 3, 4>(a, s);   // measured best for w=48 (4.60 ms vs 5.56 ms, products M=1)
+  }
   if (w4 <= 16) return launch<8, 2, 4>(a, s);
+  if (w4 <= 25) {   // w = 100 (products d0); variant 1: 6 groups x 5 lanes x 5 float4
+    static int v = -1;
+    if (v < 0) {
+      const char* e = getenv("DIGEST_SPMM_V25");
+      v = e ? atoi(e) : 0;
+    }
+    if (v == 1) return launch<5, 5, 2, false>(a, s);
+    if (v == 2) return launch<5, 5, 2, true>(a, s);
+    return launch<8, 4, 2, false>(a, s);   // measured best for w=100 (9.99 ms)
+  }
   if (w4 <= 32) return launch<8, 4, 2, false>(a, s);
   if (w4 <= 64) {
     static int v = -1;

@@ -180,11 +180,16 @@ typedef enum { DIGEST_ORDER_AUTO = 0, DIGEST_ORDER_AGG_FIRST = 1,
 digest_status digest_layer_workspace(const digest_part* part, int32_t d_in, int32_t d_out,
                                      int32_t order, size_t* saved_bytes_h,
                                      size_t* scratch_bytes_h);
+/* flags DIGEST_FWD_REUSE_SAVED (AGG_FIRST only): `saved` already holds A = P_m X_ext
+ * from an earlier call on the same inputs -- the layer-1 aggregation of the static
+ * features X_ext^(0) is the same every epoch -- so only the GEMM and
+ * the activation run. */
+enum { DIGEST_FWD_REUSE_SAVED = 1u };
 digest_status digest_layer_fwd(const digest_part* part, const float* X_local, int64_t ld_x,
                                const float* X_halo, int64_t ld_xh, const float* W,
                                int32_t d_in, int32_t d_out, int32_t act, int32_t order,
-                               float* H_out, int64_t ld_h, void* saved, void* scratch,
-                               void* stream);
+                               uint32_t flags, float* H_out, int64_t ld_h, void* saved,
+                               void* scratch, void* stream);
 /* G_out: n_local x d_out gradient of the layer output (ld_g).  H_out: the forward
  * output (its sign is the ReLU mask, ReLU'(0) := 0); ignored for ACT_NONE.
  * flags DIGEST_BWD_G_IS_D: G_out already is D = G o sigma'(Z) (H_out unused).

@@ -66,8 +66,8 @@ _SIGS = {
     "digest_store_front": ([_p, _i32, _p, _p, _p], _i32),
     "digest_store_destroy": ([_p], _i32),
     "digest_layer_workspace": ([_p, _i32, _i32, _i32, _p, _p], _i32),
-    "digest_layer_fwd": ([_p, _p, _i64, _p, _i64, _p, _i32, _i32, _i32, _i32, _p, _i64, _p, _p, _p],
-                         _i32),
+    "digest_layer_fwd": ([_p, _p, _i64, _p, _i64, _p, _i32, _i32, _i32, _i32, _u32, _p, _i64, _p, _p,
+                          _p], _i32),
     "digest_layer_bwd": ([_p, _p, _i64, _p, _i64, _p, _i32, _i32, _i32, _i32, _p, _p, _i64, _p, _i64,
                           _u32, _p, _p, _i64, _p, _i64, _p, _p], _i32),
     "digest_propagate": ([_p, _i32, _p, _i64, _p, _i64, _i32, _p, _i64, _p], _i32),
@@ -243,12 +243,15 @@ def digest_layer_workspace(part, d_in, d_out, order=ORDER_AUTO):
     return s.value, t.value
 
 
+FWD_REUSE_SAVED = 1
+
+
 def digest_layer_fwd(part, X_local, X_halo, ld_xh, W, d_in, d_out, act, order, H_out, saved,
-                     scratch, stream=None):
+                     scratch, stream=None, flags=0):
     """X_halo may be a tensor, a raw device address (the store's front buffer) or None."""
     _check(lib.digest_layer_fwd(part, ptr(X_local), ld_of(X_local), ptr(X_halo), ld_xh, ptr(W),
-                                d_in, d_out, act, order, ptr(H_out), ld_of(H_out), ptr(saved),
-                                ptr(scratch), stream_ptr(stream)))
+                                d_in, d_out, act, order, flags, ptr(H_out), ld_of(H_out),
+                                ptr(saved), ptr(scratch), stream_ptr(stream)))
 
 
 BWD_G_IS_D = 1

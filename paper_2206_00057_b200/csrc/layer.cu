@@ -142,10 +142,14 @@ digest_status digest_layer_workspace(const digest_part* part, int32_t d_in, int3
 
 digest_status digest_layer_fwd(const digest_part* p, const float* X_local, int64_t ld_x,
                                const float* X_halo, int64_t ld_xh, const float* W, int32_t d_in,
-                               int32_t d_out, int32_t act, int32_t order, float* H_out,
-                               int64_t ld_h, void* saved, void* scratch, void* stream) {
+                               int32_t d_out, int32_t act, int32_t order, uint32_t flags,
+                               float* H_out, int64_t ld_h, void* saved, void* scratch,
+                               void* stream) {
   Plan pl;
   DG_TRY(make_plan(p, d_in, d_out, order, &pl));
+  const bool reuse = (flags & DIGEST_FWD_REUSE_SAVED) != 0;
+  DG_ARG(!reuse || pl.agg_first, DIGEST_E_INVALID,
+         "DIGEST_FWD_REUSE_SAVED needs the aggregate-first order (saved holds A = P_m X_ext)");
   DG_ARG(act == DIGEST_ACT_NONE || act == DIGEST_ACT_RELU, DIGEST_E_INVALID, "bad act");
   DG_TRY(check_mat(X_local, ld_x, d_in, "X_local"));
   if (pl.h > 0) DG_TRY(check_mat(X_halo, ld_xh, d_in, "X_halo"));
@@ -157,7 +161,8 @@ digest_status digest_layer_fwd(const digest_part* p, const float* X_local, int64
   const int relu = act == DIGEST_ACT_RELU;
   if (pl.agg_first) {
     float* A = reinterpret_cast<float*>(saved);
-    DG_TRY(dg::spmm(spmm_full(p, X_local, ld_x, X_halo, ld_xh, A, pl.ldi, d_in, 0), s));
+    if (!reuse)   // A = P_m X_ext; with REUSE_SAVED the caller's static inputs were aggregated before
+      DG_TRY(dg::spmm(spmm_full(p, X_local, ld_x, X_halo, ld_xh, A, pl.ldi, d_in, 0), s));
     DG_TRY(dg::gemm(gemm_rm(A, pl.ldi, W, d_out, H_out, ld_h, pl.n, d_out, d_in, relu), s));
   } else {
     size_t off = 0;

@@ -34,6 +34,7 @@ class TrainConfig:
     normalize_pushed: bool = False
     pull_mode: int = D.PULL_FLIP
     fresh: bool = False         # zero-staleness mode (the oracle's mode='fresh')
+    cache_l1: bool = False      # aggregate the static layer-1 inputs once
 
 
 class Partition:
@@ -100,8 +101,9 @@ class DigestWorker:
         # activations, saved state, gradients
         self.H = [None] + [torch.empty(n, dims[l], device=dev) for l in range(1, self.L + 1)]
         self.saved, scratch = [None], 0
+        self._a1_ready = False
         for l in range(1, self.L + 1):
-            sv, sc = D.digest_layer_workspace(part.handle, dims[l - 1], dims[l], cfg.order)
+            sv, sc = D.digest_layer_workspace(part.handle, dims[l - 1], dims[l], self.layer_order(l))
             self.saved.append(torch.empty(max(sv, 256), dtype=torch.uint8, device=dev))
             scratch = max(scratch, sc)
         self.scratch = torch.empty(max(scratch, 256), dtype=torch.uint8, device=dev)
@@ -126,13 +128,23 @@ class DigestWorker:
             D.digest_pull(self.store, l, epoch, self.cfg.pull_mode, stream)
             self.pulls += 1
 
+    def layer_order(self, l):
+        # with the layer-1 cache the first layer is always aggregate-first: A1 = P_m X_ext^(0)
+        # depends only on static inputs, so it is aggregated once and reused every epoch
+        return D.ORDER_AGG_FIRST if (l == 1 and self.cfg.cache_l1) else self.cfg.order
+
     def forward_layer(self, l, stream=None):
         dims, cfg = self.cfg.dims, self.cfg
         xl = self.x_local if l == 1 else self.H[l - 1]
         xh, ldh = self.halo_input(l)
         act = D.ACT_RELU if l < self.L else D.ACT_NONE
+        flags = 0
+        if l == 1 and cfg.cache_l1:
+            flags = D.FWD_REUSE_SAVED if self._a1_ready else 0
+            self._a1_ready = True
         D.digest_layer_fwd(self.part.handle, xl, xh, ldh, self.W[l - 1], dims[l - 1], dims[l],
-                           act, cfg.order, self.H[l], self.saved[l], self.scratch, stream)
+                           act, self.layer_order(l), self.H[l], self.saved[l], self.scratch,
+                           stream, flags=flags)
 
     def push(self, l, epoch, stream=None):
         cfg = self.cfg
@@ -169,7 +181,8 @@ class DigestWorker:
             # G_in of layer l is produced already multiplied by 1[H^(l-1) > 0], i.e. it is
             # D^(l-1); layer l-1 then skips its own masking pass (DIGEST_BWD_G_IS_D).
             D.digest_layer_bwd(self.part.handle, xl, xh, ldh, self.W[l - 1], dims[l - 1], dims[l],
-                               act, cfg.order, self.saved[l], None, self.G[l], self.GW[l - 1],
+                               act, self.layer_order(l), self.saved[l], None, self.G[l],
+                               self.GW[l - 1],
                                self.G[l - 1] if l >= 2 else None, self.scratch, stream,
                                flags=D.BWD_G_IS_D if l < self.L else 0,
                                gin_mask=self.H[l - 1] if l >= 2 else None)

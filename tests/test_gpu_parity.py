@@ -488,3 +488,27 @@ def test_fresh_mode_vs_oracle_and_full_graph(M, pull_mode):
     for l, wref in enumerate(run.weights):
         assert rel(ws[0].W[l].cpu().numpy(), wref) <= TOL
     grp.close()
+
+
+def test_layer1_aggregation_cache_is_exact():
+    """A1 = P_m X_ext^(0) aggregated once and reused; the trajectory equals
+    the oracle's (which recomputes it every epoch)."""
+    from paper_2206_00057_b200.engine import TrainConfig, build_workers, LoopbackGroup
+    cfg = small_config(num_nodes=1000, nnz=12000, d0=36, hidden=(24,), num_classes=5, c_pad=8,
+                       seed=77, train_frac=0.5)
+    inp = make_inputs(cfg)
+    part = make_block_parts(cfg, 2)
+    tc = TrainConfig(dims=cfg.dims, num_classes=cfg.num_classes, sync_interval=2, lr=0.05,
+                     cache_l1=True)     # d0=36 > 24: layer 1 would be transform-first without it
+    ws = build_workers(inp.indptr, inp.indices, inp.x, inp.y, inp.train_mask, inp.weights, part, 2, tc)
+    grp = LoopbackGroup(ws)
+    run = oracle.oracle_train(inp.indptr, inp.indices, inp.x, inp.y, inp.train_mask, inp.weights,
+                              cfg.num_classes, part, 2, sync_interval=2, epochs=4, lr=0.05)
+    for r in range(1, 5):
+        grp.epoch(r)
+        torch.cuda.synchronize()
+        loss = sum(w.loss.item() for w in ws)
+        assert abs(loss - run.records[r - 1].loss) <= TOL * abs(run.records[r - 1].loss)
+    for l, wref in enumerate(run.weights):
+        assert rel(ws[0].W[l].cpu().numpy(), wref) <= TOL
+    grp.close()

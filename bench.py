@@ -40,6 +40,10 @@ def parse():
     ap.add_argument("--sample-frac", type=float, default=0.1,
                     help="oracle sample: fraction of nodes/edges of the workload")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sync-interval", type=int, default=0,
+                    help="override the config's N_sync (the Fig. 6 sweep, SURVEY f1)")
+    ap.add_argument("--fresh", action="store_true",
+                    help="zero-staleness exchange every level and epoch (SURVEY f1)")
     ap.add_argument("--cache-l1", action="store_true",
                     help="aggregate the static layer-1 inputs once (SURVEY f3 (i)); off by default")
     return ap.parse_args()
@@ -181,9 +185,10 @@ def run_ours(a, rank, world, local):
         comm_grad = D.digest_comm_init(ids[0], world, rank)
         comm_halo = D.digest_comm_init(ids[1], world, rank)
 
-    tc = TrainConfig(dims=cfg.dims, num_classes=cfg.num_classes, sync_interval=cfg.sync_interval,
+    n_sync = a.sync_interval or cfg.sync_interval
+    tc = TrainConfig(dims=cfg.dims, num_classes=cfg.num_classes, sync_interval=n_sync,
                      lr=0.01, optimizer="adam", async_push=(a.mode == "async"),
-                     cache_l1=a.cache_l1)
+                     cache_l1=a.cache_l1, fresh=a.fresh)
     t1 = time.time()
     (w,) = build_workers(inp.indptr, inp.indices, inp.x, inp.y, inp.train_mask, inp.weights,
                          part_of, M, tc, ranks=[rank], comm_grad=comm_grad, comm_halo=comm_halo)
@@ -289,7 +294,8 @@ def run_ours(a, rank, world, local):
             "warmup": a.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": a.config, "num_nodes": cfg.num_nodes, "nnz": cfg.nnz,
-                       "parts": M, "dims": list(cfg.dims), "sync_interval": cfg.sync_interval,
+                       "parts": M, "dims": list(cfg.dims), "sync_interval": n_sync,
+                       "fresh": a.fresh,
                        "mode": a.mode, "cache_l1": a.cache_l1,
                        "n_local": info.n_local, "n_halo": info.n_halo,
                        "nnz_local": info.nnz, "l2": "inputs larger than L2 (no flush needed)"},

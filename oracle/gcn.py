@@ -40,12 +40,17 @@ def layer_forward(part, x_local, x_halo, w, relu: bool):
     return {"A": A, "Z": Z, "H": H}
 
 
-def layer_backward(part, x_local, x_halo, w, g_out, act_mask, need_g_in: bool):
+def layer_backward(part, x_local, x_halo, w, g_out, act_mask, need_g_in: bool,
+                   need_g_halo: bool = False):
     """Eq. 6 and P:785-792 with constant halo.
 
     act_mask: boolean sigma'(Z) (None for the identity output layer).  It is passed
     in so that a caller comparing against another implementation can share that
     implementation's ReLU decisions (integer decisions taken once, in one precision).
+
+    need_g_halo: also return G_halo = P_out^T D W^T (n_halo rows), the gradient this
+    partition's rows send back to the owners of its halo nodes -- the appendix's extra
+    backward term.  It is not part of Eq. 6's constant-halo reading.
     """
     P = prop_matrix(part)
     D = np.asarray(g_out, dtype=np.float64)
@@ -53,11 +58,14 @@ def layer_backward(part, x_local, x_halo, w, g_out, act_mask, need_g_in: bool):
         D = D * np.asarray(act_mask, dtype=np.float64)
     A = P @ _x_ext(x_local, x_halo, part.n_halo)
     G_W = A.T @ D
-    G_in = None
+    G_in = G_halo = None
     if need_g_in:
         P_in = P[:, : part.n_local]
         G_in = P_in.T @ (D @ np.asarray(w, dtype=np.float64).T)
-    return {"D": D, "G_W": G_W, "G_in": G_in}
+    if need_g_halo:
+        P_out = P[:, part.n_local:]
+        G_halo = P_out.T @ (D @ np.asarray(w, dtype=np.float64).T)
+    return {"D": D, "G_W": G_W, "G_in": G_in, "G_halo": G_halo}
 
 
 def cross_entropy(logits, labels, train_mask, num_classes: int, w_loss: float):

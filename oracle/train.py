@@ -93,7 +93,13 @@ class OracleRun:
 def oracle_train(indptr, indices, x, y, train_mask, weights, num_classes, part_of,
                  num_parts, sync_interval, epochs, lr=0.01, optimizer="sgd",
                  cold_start="zero", mode="stale", normalize_pushed=False,
-                 loss_weighting="count", record_outputs=False, parts=None) -> OracleRun:
+                 loss_weighting="count", record_outputs=False, parts=None,
+                 halo_grad="none") -> OracleRun:
+    """halo_grad: 'none' (halo inputs are constants, P:810 -- the default) or
+    'same_epoch' (the appendix's P_out^T D W^T term, computed by each
+    part for its halo rows and returned to the owners in the same iteration)."""
+    if halo_grad not in ("none", "same_epoch"):
+        raise ValueError(halo_grad)
     if sync_interval < 1 or epochs < 1:
         raise ValueError("sync interval and epochs must be >= 1")
     M, Ns = num_parts, sync_interval
@@ -169,18 +175,33 @@ def oracle_train(indptr, indices, x, y, train_mask, weights, num_classes, part_o
                 pending[l] = normalize_rows(glob) if normalize_pushed else glob
                 run.push_count += M
             rec.reps[l] = glob
-        # loss, backward, AGG, update
+        # loss, backward (layer-major over the parts), AGG, update
         total = [np.zeros_like(w) for w in W]
+        g = {}
         for m, p in enumerate(parts):
-            loss, g = cross_entropy(outs[(L, m)]["H"], y[p.local_ids], train[p.local_ids],
-                                    num_classes, wl[m])
+            loss, g[m] = cross_entropy(outs[(L, m)]["H"], y[p.local_ids], train[p.local_ids],
+                                       num_classes, wl[m])
             rec.loss += loss
-            for l in range(L, 0, -1):
+        for l in range(L, 0, -1):
+            gin, ghalo = {}, {}
+            for m, p in enumerate(parts):
                 xl, xh = inputs[(l, m)]
                 mask = None if l == L else outs[(l, m)]["Z"] > 0
-                b = layer_backward(p, xl, xh, W[l - 1], g, mask, need_g_in=l >= 2)
+                b = layer_backward(p, xl, xh, W[l - 1], g[m], mask, need_g_in=l >= 2,
+                                   need_g_halo=(halo_grad == "same_epoch" and l >= 2))
                 total[l - 1] += b["G_W"]
-                g = b["G_in"]
+                gin[m], ghalo[m] = b["G_in"], b["G_halo"]
+            if l >= 2 and halo_grad == "same_epoch":
+                # P:816 term, returned in the same iteration: rows of G_halo of part m go to
+                # the owners of its halo nodes and add into their G^(l-1) before sigma'
+                for m, p in enumerate(parts):
+                    owner = np.asarray(part_of)[p.halo_ids]
+                    for k, pk in enumerate(parts):
+                        sel = np.flatnonzero(owner == k)
+                        if sel.size:
+                            loc_k = np.searchsorted(pk.local_ids, p.halo_ids[sel])
+                            np.add.at(gin[k], loc_k, ghalo[m][sel])
+            g = gin
         rec.grads = total
         if record_outputs:
             rec.part_out = outs

@@ -157,6 +157,18 @@ digest_status digest_pull(digest_store* store, int32_t level, int64_t epoch, int
  * inputs X[V_m] and X[H_m] of X_ext^(0)).  width % 4 == 0. */
 digest_status digest_gather_rows(const float* src, int64_t ld_src, const int32_t* idx, int64_t n,
                                  float* dst, int64_t ld_dst, int32_t width, void* stream);
+/* Halo-gradient return (the appendix's P_out^T D W^T term):
+ * digest_store_grad_buffer gives the store-owned n_halo x ld buffer of `level` that
+ * digest_layer_bwd fills (its G_halo output) with the gradient this part computes for
+ * its halo rows; digest_return_halo_grad then delivers every halo segment to its owner
+ * and adds it, masked by 1[mask > 0] (the owner's ReLU', NULL = unmasked), into the
+ * owner's local gradient rows G_local[send_idx] -- peer by peer in ascending order, so
+ * the result is deterministic.  Collective over the parts (loopback: linked stores). */
+digest_status digest_store_grad_buffer(digest_store* store, int32_t level, float** buf_h,
+                                       int64_t* ld_h);
+digest_status digest_return_halo_grad(digest_store* store, int32_t level, float* G_local,
+                                      int64_t ld_g, const float* mask, int64_t ld_m,
+                                      void* stream);
 /* Current front buffer, its leading dimension and the version it holds. */
 digest_status digest_store_front(const digest_store* store, int32_t level,
                                  const float** front_h, int64_t* ld_h, int64_t* version_h);
@@ -204,7 +216,10 @@ digest_status digest_layer_bwd(const digest_part* part, const float* X_local, in
                                const void* saved, const float* H_out, int64_t ld_h,
                                const float* G_out, int64_t ld_g, uint32_t flags, float* G_W,
                                float* G_in, int64_t ld_gi, const float* gin_mask,
-                               int64_t ld_gm, void* scratch, void* stream);
+                               int64_t ld_gm, float* G_halo, int64_t ld_gh, void* scratch,
+                               void* stream);
+/* G_halo (n_halo x d_in, ld_gh; NULL = skip) = P_out^T D W^T: the gradient of this
+ * part's halo rows, unmasked, for digest_return_halo_grad. */
 
 /* The propagation product alone (the aggregation of Eq. 5 / its transposes):
  *   mode 0: Y = P_m X_ext      (n_local rows; X_ext = [X_local ; X_halo], width w)

@@ -69,7 +69,9 @@ _SIGS = {
     "digest_layer_fwd": ([_p, _p, _i64, _p, _i64, _p, _i32, _i32, _i32, _i32, _u32, _p, _i64, _p, _p,
                           _p], _i32),
     "digest_layer_bwd": ([_p, _p, _i64, _p, _i64, _p, _i32, _i32, _i32, _i32, _p, _p, _i64, _p, _i64,
-                          _u32, _p, _p, _i64, _p, _i64, _p, _p], _i32),
+                          _u32, _p, _p, _i64, _p, _i64, _p, _i64, _p, _p], _i32),
+    "digest_store_grad_buffer": ([_p, _i32, _p, _p], _i32),
+    "digest_return_halo_grad": ([_p, _i32, _p, _i64, _p, _i64, _p], _i32),
     "digest_propagate": ([_p, _i32, _p, _i64, _p, _i64, _i32, _p, _i64, _p], _i32),
     "digest_xent_workspace": ([_i64, _p], _i32),
     "digest_xent": ([_p, _i64, _i32, _i64, _p, _p, _f32, _p, _i64, _p, _p, _p], _i32),
@@ -258,14 +260,30 @@ BWD_G_IS_D = 1
 
 
 def digest_layer_bwd(part, X_local, X_halo, ld_xh, W, d_in, d_out, act, order, saved, H_out,
-                     G_out, G_W, G_in, scratch, stream=None, flags=0, gin_mask=None):
+                     G_out, G_W, G_in, scratch, stream=None, flags=0, gin_mask=None,
+                     G_halo=None, ld_gh=0):
+    """G_halo may be a tensor or a raw device address (the store's gradient buffer)."""
+    if isinstance(G_halo, torch.Tensor):
+        ld_gh = ld_of(G_halo)
     _check(lib.digest_layer_bwd(part, ptr(X_local), ld_of(X_local), ptr(X_halo), ld_xh, ptr(W),
                                 d_in, d_out, act, order, ptr(saved), ptr(H_out),
                                 ld_of(H_out) if H_out is not None else 0, ptr(G_out),
                                 ld_of(G_out), flags, ptr(G_W), ptr(G_in),
                                 ld_of(G_in) if G_in is not None else 0, ptr(gin_mask),
-                                ld_of(gin_mask) if gin_mask is not None else 0, ptr(scratch),
-                                stream_ptr(stream)))
+                                ld_of(gin_mask) if gin_mask is not None else 0, ptr(G_halo),
+                                ld_gh, ptr(scratch), stream_ptr(stream)))
+
+
+def digest_store_grad_buffer(store, level):
+    p, ld = C.c_void_p(), C.c_int64()
+    _check(lib.digest_store_grad_buffer(store, level, C.byref(p), C.byref(ld)))
+    return p.value, ld.value
+
+
+def digest_return_halo_grad(store, level, G_local, mask=None, stream=None):
+    _check(lib.digest_return_halo_grad(store, level, ptr(G_local), ld_of(G_local), ptr(mask),
+                                       ld_of(mask) if mask is not None else 0,
+                                       stream_ptr(stream)))
 
 
 def digest_propagate(part, mode, X_local, X_halo, ld_xh, width, Y, stream=None):

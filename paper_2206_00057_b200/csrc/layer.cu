@@ -108,6 +108,27 @@ dg::SpmmArgs spmm_in(const digest_part* p, const float* X, int64_t ld, float* Y,
   return a;
 }
 
+// Y (n_halo rows) = P_out^T X over the reverse-halo CSR (halo row j -> local columns).
+dg::SpmmArgs spmm_rh(const digest_part* p, const float* X, int64_t ld, float* Y, int64_t ldy,
+                     int32_t w) {
+  dg::SpmmArgs a{};
+  a.row_ptr = p->rh_ptr;
+  a.in_len = nullptr;
+  a.col = p->rh_col;
+  a.val = p->rh_val;
+  a.n_rows = p->n_halo;
+  a.nnz = p->rh_nnz;
+  a.X0 = X;
+  a.ld0 = ld;
+  a.split = INT64_MAX;
+  a.X1 = X;
+  a.ld1 = ld;
+  a.Y = Y;
+  a.ldy = ldy;
+  a.width = w;
+  return a;
+}
+
 dg::GemmArgs gemm_rm(const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
                      int64_t ldc, int64_t M, int32_t N, int64_t K, int relu) {
   dg::GemmArgs g{};
@@ -182,8 +203,8 @@ digest_status digest_layer_bwd(const digest_part* p, const float* X_local, int64
                                int32_t d_out, int32_t act, int32_t order, const void* saved,
                                const float* H_out, int64_t ld_h, const float* G_out, int64_t ld_g,
                                uint32_t flags, float* G_W, float* G_in, int64_t ld_gi,
-                               const float* gin_mask, int64_t ld_gm, void* scratch,
-                               void* stream) {
+                               const float* gin_mask, int64_t ld_gm, float* G_halo,
+                               int64_t ld_gh, void* scratch, void* stream) {
   Plan pl;
   DG_TRY(make_plan(p, d_in, d_out, order, &pl));
   DG_ARG(act == DIGEST_ACT_NONE || act == DIGEST_ACT_RELU, DIGEST_E_INVALID, "bad act");
@@ -192,6 +213,8 @@ digest_status digest_layer_bwd(const digest_part* p, const float* X_local, int64
   if (act == DIGEST_ACT_RELU && !g_is_d) DG_TRY(check_mat(H_out, ld_h, d_out, "H_out"));
   if (G_in) DG_TRY(check_mat(G_in, ld_gi, d_in, "G_in"));
   if (G_in && gin_mask) DG_TRY(check_mat(gin_mask, ld_gm, d_in, "gin_mask"));
+  if (G_halo && pl.h > 0) DG_TRY(check_mat(G_halo, ld_gh, d_in, "G_halo"));
+  const bool want_halo = G_halo && pl.h > 0;
   DG_ARG(W && G_W && scratch, DIGEST_E_INVALID, "W, G_W and scratch must be non-NULL");
   cudaStream_t s = dg::as_stream(stream);
   size_t off = 0;
@@ -215,42 +238,29 @@ digest_status digest_layer_bwd(const digest_part* p, const float* X_local, int64
     void* wsc = carve(scratch, off, 0);
     dg::WgradSeg seg{A, pl.ldi, D, ldd, nullptr, 0, pl.n};
     DG_TRY(dg::wgrad(&seg, 1, d_in, d_out, G_W, wsc, s));
-    if (G_in) {
+    if (G_in || want_halo) {
       // U = D W^T : B(k, j) = W[j, k]
       dg::GemmArgs g = gemm_rm(D, ldd, W, d_out, U, pl.ldi, pl.n, d_in, d_out, 0);
       g.sBk = 1;
       g.sBj = d_out;
       DG_TRY(dg::gemm(g, s));
+    }
+    if (G_in) {
       dg::SpmmArgs a = spmm_in(p, U, pl.ldi, G_in, ld_gi, d_in);
       a.mask = gin_mask;
       a.ldm = ld_gm;
       DG_TRY(dg::spmm(a, s));
     }
+    if (want_halo)   // P:816 term for the owners of the halo rows: G_halo = P_out^T U
+      DG_TRY(dg::spmm(spmm_rh(p, U, pl.ldi, G_halo, ld_gh, d_in), s));
   } else {
     DG_TRY(check_mat(X_local, ld_x, d_in, "X_local"));
     if (pl.h > 0) DG_TRY(check_mat(X_halo, ld_xh, d_in, "X_halo"));
     float* S = carve(scratch, off, sizeof(float) * (pl.n + pl.h) * pl.ldo);
     void* wsc = carve(scratch, off, 0);
     DG_TRY(dg::spmm(spmm_in(p, D, ldd, S, pl.ldo, d_out), s));
-    if (pl.h > 0) {
-      dg::SpmmArgs a{};
-      a.row_ptr = p->rh_ptr;
-      a.in_len = nullptr;
-      a.col = p->rh_col;
-      a.val = p->rh_val;
-      a.n_rows = pl.h;
-      a.nnz = p->rh_nnz;
-      a.X0 = D;
-      a.ld0 = ldd;
-      a.split = INT64_MAX;
-      a.X1 = D;
-      a.ld1 = ldd;
-      a.Y = S + pl.n * pl.ldo;
-      a.ldy = pl.ldo;
-      a.width = d_out;
-      a.relu = 0;
-      DG_TRY(dg::spmm(a, s));
-    }
+    if (pl.h > 0)   // S_halo = P_out^T D (reverse-halo CSR, no atomics)
+      DG_TRY(dg::spmm(spmm_rh(p, D, ldd, S + pl.n * pl.ldo, pl.ldo, d_out), s));
     dg::WgradSeg segs[2] = {{X_local, ld_x, S, pl.ldo, nullptr, 0, pl.n},
                             {X_halo, ld_xh, S + pl.n * pl.ldo, pl.ldo, nullptr, 0, pl.h}};
     DG_TRY(dg::wgrad(segs, pl.h > 0 ? 2 : 1, d_in, d_out, G_W, wsc, s));
@@ -260,6 +270,13 @@ digest_status digest_layer_bwd(const digest_part* p, const float* X_local, int64
       g.sBj = d_out;
       g.mask = gin_mask;
       g.ldm = ld_gm;
+      DG_TRY(dg::gemm(g, s));
+    }
+    if (want_halo) {   // P:816 term for the owners of the halo rows: G_halo = S_halo W^T
+      dg::GemmArgs g = gemm_rm(S + pl.n * pl.ldo, pl.ldo, W, d_out, G_halo, ld_gh, pl.h, d_in,
+                               d_out, 0);
+      g.sBk = 1;
+      g.sBj = d_out;
       DG_TRY(dg::gemm(g, s));
     }
   }
@@ -278,21 +295,7 @@ digest_status digest_propagate(const digest_part* p, int32_t mode, const float* 
   cudaStream_t s = dg::as_stream(stream);
   if (mode == 0) return dg::spmm(spmm_full(p, X_local, ld_x, X_halo, ld_xh, Y, ld_y, width, 0), s);
   if (mode == 1) return dg::spmm(spmm_in(p, X_local, ld_x, Y, ld_y, width), s);
-  dg::SpmmArgs a{};
-  a.row_ptr = p->rh_ptr;
-  a.col = p->rh_col;
-  a.val = p->rh_val;
-  a.n_rows = p->n_halo;
-  a.nnz = p->rh_nnz;
-  a.X0 = X_local;
-  a.ld0 = ld_x;
-  a.split = INT64_MAX;
-  a.X1 = X_local;
-  a.ld1 = ld_x;
-  a.Y = Y;
-  a.ldy = ld_y;
-  a.width = width;
-  return dg::spmm(a, s);
+  return dg::spmm(spmm_rh(p, X_local, ld_x, Y, ld_y, width), s);
 }
 
 digest_status digest_gemm(const float* A, int64_t lda, const float* B, int64_t ldb, float* C,

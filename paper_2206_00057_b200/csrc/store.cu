@@ -30,7 +30,41 @@ struct Level {
   float* send_buf = nullptr;
   cudaEvent_t done = nullptr;   // exchange completion (async mode)
   bool inflight = false;
+  float* grad_buf = nullptr;    // n_halo x ld: gradient of this part's halo rows (P:816 term)
+  float* ret_recv = nullptr;    // n_send x ld: returned gradients received from peers (NCCL)
 };
+
+// G[idx[j]] += 1[mask[idx[j]] > 0] * src[j]  for the rows of one peer's segment (one launch
+// per peer, in ascending peer order: a local row may be a halo row of several peers, so
+// this keeps the accumulation race-free and deterministic).
+__global__ void k_return_add(const float* __restrict__ src, int64_t ld_src,
+                             const int32_t* __restrict__ idx, int64_t n, float* __restrict__ G,
+                             int64_t ld_g, const float* __restrict__ mask, int64_t ld_m, int w4) {
+  const int lane = threadIdx.x & 31;
+  int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t j = warp; j < n; j += nw) {
+    const int64_t i = idx[j];
+    const float4* s = reinterpret_cast<const float4*>(src + j * ld_src);
+    float4* g = reinterpret_cast<float4*>(G + i * ld_g);
+    const float4* m = mask ? reinterpret_cast<const float4*>(mask + i * ld_m) : nullptr;
+    for (int c = lane; c < w4; c += 32) {
+      float4 v = s[c], o = g[c];
+      if (m) {
+        const float4 mk = m[c];
+        v.x = mk.x > 0.f ? v.x : 0.f;
+        v.y = mk.y > 0.f ? v.y : 0.f;
+        v.z = mk.z > 0.f ? v.z : 0.f;
+        v.w = mk.w > 0.f ? v.w : 0.f;
+      }
+      o.x += v.x;
+      o.y += v.y;
+      o.z += v.z;
+      o.w += v.w;
+      g[c] = o;
+    }
+  }
+}
 
 struct Segs {
   float* dst[DIGEST_MAX_PARTS];
@@ -103,6 +137,8 @@ void destroy_store(digest_store* st) {
     cudaFree(L.buf[0]);
     cudaFree(L.buf[1]);
     cudaFree(L.send_buf);
+    cudaFree(L.grad_buf);
+    cudaFree(L.ret_recv);
     if (L.done) cudaEventDestroy(L.done);
   }
   if (st->packed) cudaEventDestroy(st->packed);
@@ -174,8 +210,11 @@ digest_status digest_store_create(const digest_part* part, digest_comm* comm, in
       if (cudaMemset(L.buf[b], 0, hb) != cudaSuccess)
         return fail(dg::set_error(DIGEST_E_CUDA, "cudaMemset failed"));
     }
+    if (cudaMalloc(&L.grad_buf, hb) != cudaSuccess ||
+        cudaMemset(L.grad_buf, 0, hb) != cudaSuccess)
+      return fail(dg::set_error(DIGEST_E_NOMEM, "gradient-return buffer allocation failed"));
     if (comm && comm->nranks > 1) {
-      if (cudaMalloc(&L.send_buf, sb) != cudaSuccess)
+      if (cudaMalloc(&L.send_buf, sb) != cudaSuccess || cudaMalloc(&L.ret_recv, sb) != cudaSuccess)
         return fail(dg::set_error(DIGEST_E_NOMEM, "send buffer allocation failed"));
     }
     if (cudaEventCreateWithFlags(&L.done, cudaEventDisableTiming) != cudaSuccess)
@@ -324,6 +363,64 @@ digest_status digest_store_front(const digest_store* st, int32_t level, const fl
   if (front_h) *front_h = L.buf[L.front];
   if (ld_h) *ld_h = L.ld;
   if (version_h) *version_h = L.ver[L.front];
+  return DIGEST_OK;
+}
+
+digest_status digest_store_grad_buffer(digest_store* st, int32_t level, float** buf_h,
+                                       int64_t* ld_h) {
+  Level* L;
+  DG_TRY(get_level(st, level, &L));
+  if (buf_h) *buf_h = L->grad_buf;
+  if (ld_h) *ld_h = L->ld;
+  return DIGEST_OK;
+}
+
+digest_status digest_return_halo_grad(digest_store* st, int32_t level, float* G_local,
+                                      int64_t ld_g, const float* mask, int64_t ld_m,
+                                      void* stream) {
+  Level* L;
+  DG_TRY(get_level(st, level, &L));
+  const digest_part* p = st->part;
+  DG_ARG(G_local || p->n_local == 0, DIGEST_E_INVALID, "G_local is NULL");
+  DG_ARG(ld_g >= L->width && ld_g % 4 == 0 && ((uintptr_t)G_local & 15) == 0, DIGEST_E_INVALID,
+         "G_local: ld must be >= width and a multiple of 4, pointer 16-byte aligned");
+  DG_ARG(!mask || (ld_m >= L->width && ld_m % 4 == 0 && ((uintptr_t)mask & 15) == 0),
+         DIGEST_E_INVALID, "mask: bad ld or alignment");
+  cudaStream_t s = dg::as_stream(stream);
+  const int M = p->num_parts, me = p->rank;
+  if (M == 1) return DIGEST_OK;
+  const bool nccl = st->comm && st->comm->nranks > 1;
+  if (!nccl)
+    DG_ARG((int)st->peers.size() == M, DIGEST_E_STATE,
+           "single-process store of a %d-part graph: link the stores first", M);
+  if (nccl) {   // reverse of the push: my halo segment of owner k goes back to k
+    std::vector<const float*> sp(M);
+    std::vector<float*> rp(M);
+    std::vector<int64_t> cs(M), cr(M);
+    for (int k = 0; k < M; ++k) {
+      sp[k] = L->grad_buf + p->recv_off[k] * L->ld;
+      cs[k] = p->recv_count[k] * L->ld;
+      rp[k] = L->ret_recv + p->send_off[k] * L->ld;
+      cr[k] = p->send_count[k] * L->ld;
+    }
+    DG_TRY(dg::comm_alltoallv(st->comm, sp.data(), cs.data(), rp.data(), cr.data(), s));
+  }
+  for (int k = 0; k < M; ++k) {
+    if (k == me || p->send_count[k] == 0) continue;
+    const float* src;
+    if (nccl) {
+      src = L->ret_recv + p->send_off[k] * L->ld;
+    } else {
+      digest_store* pk = st->peers[k];
+      src = pk->lev[level - 1].grad_buf + pk->part->recv_off[me] * L->ld;
+    }
+    const int64_t n = p->send_count[k];
+    int64_t blocks = dg::ceil_div(n, 8);
+    if (blocks > dg::num_sms() * 16) blocks = dg::num_sms() * 16;
+    DG_LAUNCH(DIGEST_PROF_PACK, s, 12.0 * n * L->width, 0, k_return_add, (unsigned)blocks, 256, 0,
+              src, L->ld, p->send_idx + p->send_off[k], n, G_local, ld_g, mask, ld_m,
+              L->width / 4);
+  }
   return DIGEST_OK;
 }
 

@@ -35,6 +35,7 @@ class TrainConfig:
     pull_mode: int = D.PULL_FLIP
     fresh: bool = False         # zero-staleness mode (the oracle's mode='fresh')
     cache_l1: bool = False      # aggregate the static layer-1 inputs once
+    halo_grad: bool = False     # return P_out^T D W^T to the halo owners
 
 
 class Partition:
@@ -170,22 +171,37 @@ class DigestWorker:
                 D.digest_pull(self.store, l, epoch + 1, self.cfg.pull_mode, stream)
                 self.pulls += 1
 
-    def loss_and_backward(self, stream=None):
-        dims, cfg = self.cfg.dims, self.cfg
+    def compute_loss(self, stream=None):
+        cfg = self.cfg
         D.digest_xent(self.H[self.L], cfg.num_classes, self.labels, self.train_mask, self.w_loss,
                       self.G[self.L], self.loss, self.xent_scratch, stream)
+
+    def backward_layer(self, l, stream=None):
+        dims = self.cfg.dims
+        xl = self.x_local if l == 1 else self.H[l - 1]
+        xh, ldh = self.halo_input(l)
+        act = D.ACT_RELU if l < self.L else D.ACT_NONE
+        gh, ldgh = None, 0
+        if self.cfg.halo_grad and l >= 2 and self.part.n_halo > 0:
+            gh, ldgh = D.digest_store_grad_buffer(self.store, l - 1)
+        # G_in of layer l is produced already multiplied by 1[H^(l-1) > 0], i.e. it is
+        # D^(l-1); layer l-1 then skips its own masking pass (DIGEST_BWD_G_IS_D).
+        D.digest_layer_bwd(self.part.handle, xl, xh, ldh, self.W[l - 1], dims[l - 1], dims[l],
+                           act, self.layer_order(l), self.saved[l], None, self.G[l],
+                           self.GW[l - 1], self.G[l - 1] if l >= 2 else None, self.scratch,
+                           stream, flags=D.BWD_G_IS_D if l < self.L else 0,
+                           gin_mask=self.H[l - 1] if l >= 2 else None, G_halo=gh, ld_gh=ldgh)
+
+    def return_halo_grad(self, l, stream=None):
+        """Add the peers' G_halo rows for my nodes into D^(l-1)."""
+        D.digest_return_halo_grad(self.store, l - 1, self.G[l - 1], self.H[l - 1], stream)
+
+    def loss_and_backward(self, stream=None):
+        self.compute_loss(stream)
         for l in range(self.L, 0, -1):
-            xl = self.x_local if l == 1 else self.H[l - 1]
-            xh, ldh = self.halo_input(l)
-            act = D.ACT_RELU if l < self.L else D.ACT_NONE
-            # G_in of layer l is produced already multiplied by 1[H^(l-1) > 0], i.e. it is
-            # D^(l-1); layer l-1 then skips its own masking pass (DIGEST_BWD_G_IS_D).
-            D.digest_layer_bwd(self.part.handle, xl, xh, ldh, self.W[l - 1], dims[l - 1], dims[l],
-                               act, self.layer_order(l), self.saved[l], None, self.G[l],
-                               self.GW[l - 1],
-                               self.G[l - 1] if l >= 2 else None, self.scratch, stream,
-                               flags=D.BWD_G_IS_D if l < self.L else 0,
-                               gin_mask=self.H[l - 1] if l >= 2 else None)
+            self.backward_layer(l, stream)
+            if self.cfg.halo_grad and l >= 2:
+                self.return_halo_grad(l, stream)   # collective (NCCL) per level
 
     def allreduce(self, stream=None):
         D.digest_grad_allreduce(self.comm_grad, self.G_flat, 1.0, stream)
@@ -244,8 +260,19 @@ class LoopbackGroup:
                     w.pull(r, stream)
             for w in self.workers:
                 w.forward(r, sched.push(r), stream)
-        for w in self.workers:
-            w.loss_and_backward(stream)
+        if self.workers[0].cfg.halo_grad:
+            # layer-major: every part's G_halo of layer l exists before any owner adds it
+            for w in self.workers:
+                w.compute_loss(stream)
+            for l in range(self.workers[0].L, 0, -1):
+                for w in self.workers:
+                    w.backward_layer(l, stream)
+                if l >= 2:
+                    for w in self.workers:
+                        w.return_halo_grad(l, stream)
+        else:
+            for w in self.workers:
+                w.loss_and_backward(stream)
         if len(self.workers) > 1:
             D.digest_grad_allreduce_local([w.G_flat for w in self.workers], 1.0, stream)
         for w in self.workers:

@@ -1,0 +1,87 @@
+"""GPU path vs oracle for the halo-gradient return (the P:816 term)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from oracle.gcn import layer_backward, cross_entropy
+from oracle.train import full_prop_matrix, full_graph_forward, full_graph_backward
+from synth import make_graph, make_inputs, make_random_parts, small_config
+from tests.test_gpu_parity import D, TOL, gpu_partition, rel
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+
+
+@pytest.mark.parametrize("d_in,d_out,order", [(24, 40, 1), (40, 24, 2), (256, 48, 0),
+                                              (100, 256, 0)])
+def test_g_halo_per_call(d_in, d_out, order):
+    Dm = D()
+    cfg = small_config(num_nodes=900, nnz=9000, d0=d_in, hidden=(d_out,), seed=5 + d_in)
+    ip, ix = make_graph(cfg)
+    part = make_random_parts(cfg.num_nodes, 3, 1)
+    p, _ = gpu_partition(ip, ix, part, 3, 2)
+    op = oracle.oracle_partition(ip, ix, part, 3, 2)
+    g = torch.Generator().manual_seed(d_in + d_out)
+    xl = torch.rand(p.n_local, d_in, generator=g) * 2 - 1
+    xh = torch.rand(p.n_halo, d_in, generator=g) * 2 - 1
+    w = (torch.rand(d_in, d_out, generator=g) * 2 - 1) / np.sqrt(d_in)
+    gout = torch.randn(p.n_local, d_out, generator=g)
+    sv, sc = Dm.digest_layer_workspace(p.handle, d_in, d_out, order)
+    saved = torch.empty(max(sv, 256), dtype=torch.uint8, device="cuda")
+    scratch = torch.empty(max(sc, 256), dtype=torch.uint8, device="cuda")
+    H = torch.empty(p.n_local, d_out, device="cuda")
+    Dm.digest_layer_fwd(p.handle, xl.cuda(), xh.cuda(), d_in, w.cuda(), d_in, d_out, 1, order, H,
+                        saved, scratch)
+    GW = torch.empty(d_in, d_out, device="cuda")
+    Gin = torch.empty(p.n_local, d_in, device="cuda")
+    Gh = torch.full((p.n_halo, d_in), 9.0, device="cuda")
+    Dm.digest_layer_bwd(p.handle, xl.cuda(), xh.cuda(), d_in, w.cuda(), d_in, d_out, 1, order,
+                        saved, H, gout.cuda(), GW, Gin, scratch, G_halo=Gh)
+    torch.cuda.synchronize()
+    b = layer_backward(op, xl.numpy(), xh.numpy(), w.numpy(), gout.numpy(),
+                       H.cpu().numpy() > 0, True, need_g_halo=True)
+    assert rel(Gh.cpu().numpy(), b["G_halo"]) <= TOL
+    assert rel(GW.cpu().numpy(), b["G_W"]) <= TOL
+    p.close()
+
+
+@pytest.mark.parametrize("M,fresh,N", [(2, True, 1), (3, True, 1), (3, False, 2)])
+def test_trajectory_with_halo_grad(M, fresh, N):
+    from paper_2206_00057_b200.engine import TrainConfig, build_workers, LoopbackGroup
+    cfg = small_config(num_nodes=1000, nnz=11000, d0=20, hidden=(32, 16), num_classes=6, c_pad=8,
+                       seed=60 + M, train_frac=0.5)
+    inp = make_inputs(cfg)
+    part = make_random_parts(cfg.num_nodes, M, 9)
+    tc = TrainConfig(dims=cfg.dims, num_classes=cfg.num_classes, sync_interval=N, lr=0.05,
+                     fresh=fresh, halo_grad=True)
+    ws = build_workers(inp.indptr, inp.indices, inp.x, inp.y, inp.train_mask, inp.weights, part, M, tc)
+    grp = LoopbackGroup(ws)
+    R = 3
+    run = oracle.oracle_train(inp.indptr, inp.indices, inp.x, inp.y, inp.train_mask, inp.weights,
+                              cfg.num_classes, part, M, sync_interval=N, epochs=R, lr=0.05,
+                              mode="fresh" if fresh else "stale", halo_grad="same_epoch")
+    for r in range(1, R + 1):
+        grp.epoch(r)
+        torch.cuda.synchronize()
+        loss = sum(w.loss.item() for w in ws)
+        assert abs(loss - run.records[r - 1].loss) <= TOL * abs(run.records[r - 1].loss)
+        if r == 1 and fresh:
+            # exact: every layer's aggregated gradient equals full-graph GCN's (A16 closed)
+            P = full_prop_matrix(inp.indptr, inp.indices)
+            W = [x.astype(np.float64) for x in inp.weights]
+            H, Z = full_graph_forward(P, inp.x, W)
+            _, g = cross_entropy(H[-1], inp.y, inp.train_mask, cfg.num_classes,
+                                 1.0 / inp.train_mask.sum())
+            ref = full_graph_backward(P, H, Z, W, g)
+            for l, gref in enumerate(ref):
+                assert rel(ws[0].GW[l].cpu().numpy(), gref) <= TOL, l
+    for l, wref in enumerate(run.weights):
+        assert rel(ws[0].W[l].cpu().numpy(), wref) <= TOL
+    grp.close()

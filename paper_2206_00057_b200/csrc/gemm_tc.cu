@@ -62,7 +62,8 @@ struct Cfg {
   static constexpr uint32_t B_BYTES = BN * kBK * 4;
   static constexpr uint32_t STAGE = 2 * A_BYTES + 2 * B_BYTES;
   static constexpr int STAGES = (200 * 1024 / STAGE) > 4 ? 4 : (200 * 1024 / STAGE);
-  static constexpr uint32_t SMEM = STAGES * STAGE + 1024 + 256;
+  static constexpr uint32_t EPI = 4 * 4096;                 // per-warp epilogue staging
+  static constexpr uint32_t SMEM = STAGES * STAGE + EPI + 1024 + 256;
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
   static_assert(B_BYTES % 1024 == 0, "1024-byte aligned stages (SW128 atoms)");
 };
@@ -77,7 +78,8 @@ k_gemm_tf32x3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * G::STAGE);
+  uint8_t* epi = smem + S * G::STAGE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(epi + G::EPI);
   uint64_t* full = bars;
   uint64_t* conv = bars + S;
   uint64_t* empty = bars + 2 * S;
@@ -199,37 +201,47 @@ k_gemm_tf32x3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       const int n0 = (int)((t % n_tiles_n) * BN);
       tc::mbar_wait(&tfull[acc], aph);
       tc::tc_fence_after();
-      const int64_t row = m0 + q * 32 + lane;
+      // TMEM gives lane l the 32 columns of row l; stage them through a per-warp
+      // 32 x 128 B shared buffer (16 B chunks XOR-swizzled by row, conflict-free) so
+      // the global stores are full 128 B lines: 4 rows x 8 chunks per warp store.
+      float4* stg = reinterpret_cast<float4*>(epi + q * 4096);
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
         uint32_t r[32];
         tc::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * G::ACC + c0, r);
         tc::tmem_ld_wait();
-        if (row < M) {
-          float* crow = C + row * ldc + n0 + c0;
 #pragma unroll
-          for (int j = 0; j < 32; j += 4) {
-            if (n0 + c0 + j < N) {
-              float4 v = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
-                                     __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
-              if (relu) {
-                v.x = fmaxf(v.x, 0.f);
-                v.y = fmaxf(v.y, 0.f);
-                v.z = fmaxf(v.z, 0.f);
-                v.w = fmaxf(v.w, 0.f);
-              }
-              if (mask) {
-                const float4 mk =
-                    __ldg(reinterpret_cast<const float4*>(mask + row * ldm + n0 + c0 + j));
-                v.x = mk.x > 0.f ? v.x : 0.f;
-                v.y = mk.y > 0.f ? v.y : 0.f;
-                v.z = mk.z > 0.f ? v.z : 0.f;
-                v.w = mk.w > 0.f ? v.w : 0.f;
-              }
-              *reinterpret_cast<float4*>(crow + j) = v;
+        for (int j = 0; j < 8; ++j) {
+          float4 v = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                 __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+          if (relu) {
+            v.x = fmaxf(v.x, 0.f);
+            v.y = fmaxf(v.y, 0.f);
+            v.z = fmaxf(v.z, 0.f);
+            v.w = fmaxf(v.w, 0.f);
+          }
+          stg[lane * 8 + (j ^ (lane & 7))] = v;
+        }
+        __syncwarp();
+        const int ch = lane & 7;
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int rr = it * 4 + (lane >> 3);
+          const int64_t row = m0 + q * 32 + rr;
+          const int col = n0 + c0 + 4 * ch;
+          if (row < M && col < N) {
+            float4 v = stg[rr * 8 + (ch ^ (rr & 7))];
+            if (mask) {
+              const float4 mk = __ldg(reinterpret_cast<const float4*>(mask + row * ldm + col));
+              v.x = mk.x > 0.f ? v.x : 0.f;
+              v.y = mk.y > 0.f ? v.y : 0.f;
+              v.z = mk.z > 0.f ? v.z : 0.f;
+              v.w = mk.w > 0.f ? v.w : 0.f;
             }
+            *reinterpret_cast<float4*>(C + row * ldc + col) = v;
           }
         }
+        __syncwarp();
       }
       tc::tc_fence_before();
       tc::mbar_arrive(&tempty[acc]);

@@ -5,10 +5,10 @@
 // partition (up to 2.45M).  Both operands are row-major [K x M] / [K x N], i.e.
 // MN-major for UMMA.  Measured on B200 (tools/umma_probe2.cu): kind::tf32 ignores
 // MN-major operands (the MMA writes nothing), kind::f16 accepts them.  So this
-// kernel splits each fp32 value into three bf16 pieces x = b0 + b1 + b2 (exact to
-// ~2^-27) and accumulates the six products with >= 2^-24 weight
-// (b2c0 + b0c2 + b1c1 + b1c0 + b0c1 + b0c0) with kind::f16 -- the same tensor
-// time as 3xTF32 (bf16 runs at twice the TF32 rate).  TMA loads 32-float x 16-row
+// kernel splits each fp32 value into three bf16 pieces x = b0 + b1 + b2 (exactly, by
+// truncation: |b1| < 2^-7 |x|, |b2| < 2^-15 |x|) and accumulates the six products
+// b2c0 + b0c2 + b1c1 + b1c0 + b0c1 + b0c0 with kind::f16 (dropped terms <= 2^-22
+// relative) -- the same tensor time as 3xTF32 (bf16 runs at twice the TF32 rate).  TMA loads 32-float x 16-row
 // fp32 boxes (128B swizzle); split workers write the pieces in the bf16 MN-major
 // SW128 canonical layout (64-element runs, LBO = next 64-run group, SBO = next
 // 8-row K group).
@@ -46,13 +46,20 @@ struct WCfg {
   static constexpr uint32_t GRP = 64 * kBK * 2;         // one bf16 64-run group x 16 rows: 2 KB
   static constexpr uint32_t PA = AG * GRP;              // one bf16 piece of A
   static constexpr uint32_t PB = BG * GRP;              // one bf16 piece of B
-  static constexpr uint32_t STAGE = RAW_A + RAW_B + 3 * PA + 3 * PB;
-  static constexpr int STAGES = (200 * 1024 / STAGE) > 4 ? 4 : (200 * 1024 / STAGE);
-  static constexpr uint32_t SMEM = STAGES * STAGE + 1024 + 256;
+  // Two decoupled rings: fp32 TMA staging (RS deep) -> split workers -> bf16 pieces
+  // (PS deep, read by the MMA), so the TMA runs ahead of the conversion.
+  static constexpr uint32_t RAW = RAW_A + RAW_B;
+  static constexpr uint32_t PIECE = 3 * PA + 3 * PB;
+  static constexpr int PS = 2;
+  static constexpr int RS = ((200 * 1024 - PS * PIECE) / RAW) > 4 ? 4
+                                                                   : ((200 * 1024 - PS * PIECE) / RAW);
+  static constexpr uint32_t SMEM = RS * RAW + PS * PIECE + 1024 + 256;
+  static_assert(RS >= 2, "staging ring");
   static constexpr uint32_t TMEM_COLS = pow2_cols(MT * BN);
   static constexpr uint32_t BOX = 32 * kBK * 4;         // one 32-float x 16-row fp32 box: 2 KB
   static_assert(BN % 32 == 0 && BN <= 256 && MT * BN <= 512, "tile");
-  static_assert(STAGE % 1024 == 0 && RAW_B % 1024 == 0, "1024-byte aligned swizzle atoms");
+  static_assert(RAW % 1024 == 0 && PIECE % 1024 == 0 && RAW_B % 1024 == 0,
+                "1024-byte aligned swizzle atoms");
 };
 
 // Instruction descriptor, kind::f16 with bf16 A/B (format 1), fp32 D, MN-major A and B.
@@ -80,21 +87,25 @@ __device__ __forceinline__ void split8(const uint8_t* raw, uint8_t* p0, uint8_t*
   const float4 u = *reinterpret_cast<const float4*>(src + ((((e & 31) >> 2) ^ sw) << 4));
   const float4 w = *reinterpret_cast<const float4*>(src + (((((e & 31) >> 2) + 1) ^ sw) << 4));
   const float x[8] = {u.x, u.y, u.z, u.w, w.x, w.y, w.z, w.w};
+  // Truncation split (bit masks, full-rate ALU; no conversion-unit instructions):
+  // b0 = top 8 significant bits of x, r1 = x - b0 (exact, <= 16 bits), b1 = top 8 bits
+  // of r1, r2 = r1 - b1 (exact, <= 8 bits) = b2.  x = b0 + b1 + b2 exactly, and each
+  // piece is its fp32 pattern's high half, so packing is a byte permute.
+  uint32_t h0[8], h1[8], h2[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t xb = __float_as_uint(x[i]);
+    h0[i] = xb & 0xffff0000u;
+    const float r1 = x[i] - __uint_as_float(h0[i]);
+    h1[i] = __float_as_uint(r1) & 0xffff0000u;
+    h2[i] = __float_as_uint(r1 - __uint_as_float(h1[i]));
+  }
   uint32_t q0[4], q1[4], q2[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    __nv_bfloat16 h0[2], h1[2], h2[2];
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const float v = x[2 * i + j];
-      h0[j] = __float2bfloat16_rn(v);
-      const float r1 = v - __bfloat162float(h0[j]);
-      h1[j] = __float2bfloat16_rn(r1);
-      h2[j] = __float2bfloat16_rn(r1 - __bfloat162float(h1[j]));
-    }
-    q0[i] = (uint32_t)__bfloat16_as_ushort(h0[0]) | ((uint32_t)__bfloat16_as_ushort(h0[1]) << 16);
-    q1[i] = (uint32_t)__bfloat16_as_ushort(h1[0]) | ((uint32_t)__bfloat16_as_ushort(h1[1]) << 16);
-    q2[i] = (uint32_t)__bfloat16_as_ushort(h2[0]) | ((uint32_t)__bfloat16_as_ushort(h2[1]) << 16);
+    q0[i] = __byte_perm(h0[2 * i], h0[2 * i + 1], 0x7632);
+    q1[i] = __byte_perm(h1[2 * i], h1[2 * i + 1], 0x7632);
+    q2[i] = __byte_perm(h2[2 * i], h2[2 * i + 1], 0x7632);
   }
   const uint32_t off = (e >> 6) * (64 * kBK * 2) + k * 128 + ((((e & 63) >> 3) ^ sw) << 4);
   *reinterpret_cast<uint4*>(p0 + off) = make_uint4(q0[0], q0[1], q0[2], q0[3]);
@@ -106,25 +117,26 @@ __device__ __forceinline__ void split8(const uint8_t* raw, uint8_t* p0, uint8_t*
 template <int MT, int BN>
 __global__ void __launch_bounds__(kThreads, 1)
 k_wgrad_bf16x6(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-               int64_t K, int64_t k_per_cta, int M, int N, float* __restrict__ partial) {
+               int64_t K, int64_t k_per_cta, int M, int N, float* __restrict__ partial,
+               int dbg) {
   using G = WCfg<MT, BN>;
-  constexpr int S = G::STAGES;
+  constexpr int RS = G::RS, PS = G::PS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * G::STAGE);
-  uint64_t* full = bars;
-  uint64_t* conv = bars + S;
-  uint64_t* empty = bars + 2 * S;
-  uint64_t* tfull = bars + 3 * S;
-  uint64_t* tempty = bars + 3 * S + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 2);
-  auto rawA = [&](int s) { return smem + s * G::STAGE; };
-  auto rawB = [&](int s) { return smem + s * G::STAGE + G::RAW_A; };
-  auto pieceA = [&](int s, int p) { return smem + s * G::STAGE + G::RAW_A + G::RAW_B + p * G::PA; };
-  auto pieceB = [&](int s, int p) {
-    return smem + s * G::STAGE + G::RAW_A + G::RAW_B + 3 * G::PA + p * G::PB;
-  };
+  uint8_t* pieces = smem + RS * G::RAW;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(pieces + PS * G::PIECE);
+  uint64_t* full = bars;              // TMA -> split workers        [RS]
+  uint64_t* rfree = bars + RS;        // split workers -> TMA        [RS]
+  uint64_t* conv = bars + 2 * RS;     // split workers -> MMA        [PS]
+  uint64_t* empty = conv + PS;        // MMA (commit) -> split workers [PS]
+  uint64_t* tfull = empty + PS;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  auto rawA = [&](int r) { return smem + r * G::RAW; };
+  auto rawB = [&](int r) { return smem + r * G::RAW + G::RAW_A; };
+  auto pieceA = [&](int s, int p) { return pieces + s * G::PIECE + p * G::PA; };
+  auto pieceB = [&](int s, int p) { return pieces + s * G::PIECE + 3 * G::PA + p * G::PB; };
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m_base = blockIdx.y * (MT * 128);
@@ -135,8 +147,11 @@ k_wgrad_bf16x6(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   float* out = partial + ((int64_t)blockIdx.x * gridDim.y + blockIdx.y) * (int64_t)(MT * 128) * BN;
 
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < S; ++s) {
-      tc::mbar_init(&full[s], 1);
+    for (int r = 0; r < RS; ++r) {
+      tc::mbar_init(&full[r], 1);
+      tc::mbar_init(&rfree[r], 128);
+    }
+    for (int s = 0; s < PS; ++s) {
       tc::mbar_init(&conv[s], 128);
       tc::mbar_init(&empty[s], 1);
     }
@@ -154,19 +169,23 @@ k_wgrad_bf16x6(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 
   if (warp == 0) {
     if (lane == 0) {  // TMA producer: fp32 boxes, 32 MN elements x 16 K rows each
-      int s = 0;
+      int r = 0;
       uint32_t ph = 0;
       for (int kb = 0; kb < nkb; ++kb) {
         const int k0 = (int)(k_begin + (int64_t)kb * kBK);
-        tc::mbar_wait(&empty[s], ph ^ 1);
-        tc::mbar_arrive_expect_tx(&full[s], G::RAW_A + G::RAW_B);
+        tc::mbar_wait(&rfree[r], ph ^ 1);
+        if (dbg & 4) {   // timing experiment: no TMA traffic
+          tc::mbar_arrive(&full[r]);
+        } else {
+          tc::mbar_arrive_expect_tx(&full[r], G::RAW_A + G::RAW_B);
 #pragma unroll
-        for (int j = 0; j < MT * 4; ++j)
-          tc::tma_load_2d(rawA(s) + j * G::BOX, &tmA, &full[s], m_base + 32 * j, k0);
+          for (int j = 0; j < MT * 4; ++j)
+            tc::tma_load_2d(rawA(r) + j * G::BOX, &tmA, &full[r], m_base + 32 * j, k0);
 #pragma unroll
-        for (int j = 0; j < BN / 32; ++j)
-          tc::tma_load_2d(rawB(s) + j * G::BOX, &tmB, &full[s], 32 * j, k0);
-        if (++s == S) { s = 0; ph ^= 1; }
+          for (int j = 0; j < BN / 32; ++j)
+            tc::tma_load_2d(rawB(r) + j * G::BOX, &tmB, &full[r], 32 * j, k0);
+        }
+        if (++r == RS) { r = 0; ph ^= 1; }
       }
     }
   } else if (warp == 1) {
@@ -192,11 +211,11 @@ k_wgrad_bf16x6(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
               const uint64_t dA = tc::smem_desc_sw128(
                   tc::smem_u32(pieceA(s, pa[t]) + h * 2 * G::GRP), G::GRP, 1024);
               const uint64_t dB = tc::smem_desc_sw128(tc::smem_u32(pieceB(s, pb[t])), G::GRP, 1024);
-              mma_bf16(d, dA, dB, idesc, (kb != kb_first) || t != 0);
+              if (!(dbg & 2)) mma_bf16(d, dA, dB, idesc, (kb != kb_first) || t != 0);
             }
           }
           tc::mma_commit(&empty[s]);
-          if (++s == S) { s = 0; ph ^= 1; }
+          if (++s == PS) { s = 0; ph ^= 1; }
         }
         tc::mma_commit(tfull);
       }
@@ -205,21 +224,24 @@ k_wgrad_bf16x6(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const int tid = threadIdx.x - 64;
     constexpr int UA = kBK * (MT * 128 / 8);   // 8-element units of A per stage
     constexpr int UB = kBK * (BN / 8);
-    int s = 0;
-    uint32_t ph = 0;
+    int r = 0, s = 0;
+    uint32_t rph = 0, ph = 0;
     for (int kb = 0; kb < nkb; ++kb) {
-      tc::mbar_wait(&full[s], ph);
-      for (int u = tid; u < UA; u += 128) {
+      tc::mbar_wait(&full[r], rph);
+      tc::mbar_wait(&empty[s], ph ^ 1);   // the MMA has finished reading piece slot s
+      for (int u = tid; u < ((dbg & 1) ? 0 : UA); u += 128) {
         const int k = u / (MT * 128 / 8), e = (u % (MT * 128 / 8)) * 8;
-        split8(rawA(s), pieceA(s, 0), pieceA(s, 1), pieceA(s, 2), G::PA, k, e);
+        split8(rawA(r), pieceA(s, 0), pieceA(s, 1), pieceA(s, 2), G::PA, k, e);
       }
-      for (int u = tid; u < UB; u += 128) {
+      for (int u = tid; u < ((dbg & 1) ? 0 : UB); u += 128) {
         const int k = u / (BN / 8), e = (u % (BN / 8)) * 8;
-        split8(rawB(s), pieceB(s, 0), pieceB(s, 1), pieceB(s, 2), G::PB, k, e);
+        split8(rawB(r), pieceB(s, 0), pieceB(s, 1), pieceB(s, 2), G::PB, k, e);
       }
+      tc::mbar_arrive(&rfree[r]);          // staging slot r may be refilled by TMA
       tc::fence_proxy_async_smem();
       tc::mbar_arrive(&conv[s]);
-      if (++s == S) { s = 0; ph ^= 1; }
+      if (++r == RS) { r = 0; rph ^= 1; }
+      if (++s == PS) { s = 0; ph ^= 1; }
     }
   } else {  // epilogue: flush each chunk into the fp32 partial (RN adds)
     const int q = warp & 3;
@@ -285,6 +307,15 @@ __global__ void k_wgrad_reduce(const float* __restrict__ partial, int nz, int MT
   }
 }
 
+int wgrad_dbg() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DIGEST_WGRAD_DBG");   // timing experiments only (wrong results)
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
 template <int MT, int BN>
 digest_status launch_seg(const WgradSeg& sg, int M, int N, int grid_x, float* partial,
                          cudaStream_t s) {
@@ -305,7 +336,7 @@ digest_status launch_seg(const WgradSeg& sg, int M, int N, int grid_x, float* pa
   const double flops = 2.0 * (double)M * N * sg.K;
   const double bytes = 4.0 * (double)sg.K * (M + N);
   DG_LAUNCH(DIGEST_PROF_GEMM, s, bytes, flops, (k_wgrad_bf16x6<MT, BN>), grid, kThreads, G::SMEM,
-            tA, tB, sg.K, kpc, M, N, partial);
+            tA, tB, sg.K, kpc, M, N, partial, wgrad_dbg());
   return DIGEST_OK;
 }
 

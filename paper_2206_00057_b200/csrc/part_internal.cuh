@@ -8,12 +8,13 @@ struct digest_part {
   int64_t num_nodes = 0, n_local = 0, n_halo = 0, nnz = 0, nnz_in = 0, n_send = 0, rh_nnz = 0;
   int32_t num_parts = 0, rank = 0;
   int64_t max_row = 0, max_rh_row = 0;
+  int64_t hot_rows = 0;          // extended columns flagged (bit 31 of col/rh_col) as L2-hot
   std::vector<int64_t> send_count, send_off, recv_count, recv_off;
   // device arrays, owned
   int32_t* local_ids = nullptr;  // [n_local]
   int32_t* halo_ids = nullptr;   // [n_halo]
   int64_t* row_ptr = nullptr;    // [n_local+1]
-  int32_t* col = nullptr;        // [nnz] extended column
+  int32_t* col = nullptr;        // [nnz] extended column | bit 31: L2-hot source row
   float* val = nullptr;          // [nnz]
   int32_t* in_len = nullptr;     // [n_local] entries with col < n_local (they come first)
   int32_t* send_idx = nullptr;   // [n_send]

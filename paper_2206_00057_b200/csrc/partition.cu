@@ -251,6 +251,38 @@ __global__ void k_count_lt(const int32_t* __restrict__ col, int64_t nnz, int64_t
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
 }
 
+constexpr int kDegBins = 1 << 16;   // degrees >= 65535 share the top bin
+
+// Global degree of every extended column (local rows, then halo rows) + a histogram.
+__global__ void k_ext_degree(const int32_t* __restrict__ local_ids, int64_t n,
+                             const int32_t* __restrict__ halo_ids, int64_t h,
+                             const int64_t* __restrict__ indptr, int32_t* __restrict__ dext,
+                             unsigned int* __restrict__ hist) {
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n + h;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = c < n ? local_ids[c] : halo_ids[c - n];
+    int64_t d = indptr[v + 1] - indptr[v];
+    if (d >= kDegBins) d = kDegBins - 1;
+    dext[c] = (int32_t)d;
+    atomicAdd(&hist[d], 1u);
+  }
+}
+
+__global__ void k_mark_hot(int32_t* __restrict__ col, int64_t nnz, const int32_t* __restrict__ dext,
+                           int thr) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t c = col[e];
+    if (dext[c] >= thr) col[e] = (int32_t)((uint32_t)c | 0x80000000u);
+  }
+}
+
+__global__ void k_clear_hot(int32_t* __restrict__ col, int64_t nnz) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x)
+    col[e] &= 0x7fffffff;
+}
+
 __global__ void k_max_row(const int64_t* __restrict__ ptr, int64_t n, unsigned long long* out) {
   unsigned long long m = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -424,6 +456,43 @@ digest_status build(int64_t N, int64_t nnz, const int64_t* indptr, const int32_t
   P->nnz_in = (int64_t)hs[0];
   P->max_row = (int64_t)hs[1];
   P->max_rh_row = (int64_t)hs[2];
+
+  // L2 residency hint (not part of the exported layout): mark, in bit 31 of the
+  // internal column arrays, the entries whose source row belongs to the ~hot_rows
+  // highest-degree nodes of the extended column space.  The SpMM gathers those rows
+  // with an L2 evict_last policy and all others with evict_first, so the most
+  // re-read rows (a node's row is gathered deg+1 times) stay cached.  Export clears it.
+  int64_t hot_rows = 98304;   // measured best on products M=1 (w=256 SpMM 20.0 -> 17.8 ms)
+  if (const char* e = getenv("DIGEST_HOT_ROWS")) hot_rows = atoll(e);
+  const int64_t next = n_local + h;
+  if (hot_rows > 0 && next > 0) {
+    int32_t* dext;
+    unsigned int* hist;
+    DG_TRY(t.alloc(&dext, next));
+    DG_TRY(t.alloc(&hist, kDegBins));
+    DG_CUDA(cudaMemsetAsync(hist, 0, sizeof(unsigned int) * kDegBins, s));
+    DG_LAUNCH(DIGEST_PROF_OTHER, s, 0, 0, k_ext_degree, grid, block, 0, P->local_ids, n_local,
+              P->halo_ids, h, indptr, dext, hist);
+    std::vector<unsigned int> hh(kDegBins);
+    DG_CUDA(cudaMemcpyAsync(hh.data(), hist, sizeof(unsigned int) * kDegBins,
+                            cudaMemcpyDeviceToHost, s));
+    DG_CUDA(cudaStreamSynchronize(s));
+    int thr = kDegBins;   // smallest degree bin whose cumulative count stays <= hot_rows
+    int64_t cum = 0;
+    for (int b = kDegBins - 1; b >= 1; --b) {
+      if (cum + hh[b] > hot_rows) break;
+      cum += hh[b];
+      thr = b;
+    }
+    if (thr < kDegBins) {
+      DG_LAUNCH(DIGEST_PROF_OTHER, s, 0, 0, k_mark_hot, grid, block, 0, P->col, nnz_m, dext, thr);
+      if (P->rh_nnz > 0)
+        DG_LAUNCH(DIGEST_PROF_OTHER, s, 0, 0, k_mark_hot, grid, block, 0, P->rh_col, P->rh_nnz,
+                  dext, thr);
+      P->hot_rows = cum;
+    }
+    DG_CUDA(cudaStreamSynchronize(s));
+  }
   return DIGEST_OK;
 }
 
@@ -488,10 +557,15 @@ digest_status digest_part_export(const digest_part* p, int32_t* local_ids, int32
   DG_CUDA(cp(halo_ids, p->halo_ids, 4 * p->n_halo));
   DG_CUDA(cp(row_ptr, p->row_ptr, 8 * (p->n_local + 1)));
   DG_CUDA(cp(col, p->col, 4 * p->nnz));
+  if (col && p->nnz > 0)   // drop the internal L2-hint bit: the exported layout is exact
+    DG_LAUNCH(DIGEST_PROF_OTHER, s, 0, 0, k_clear_hot, dg::num_sms() * 4, 256, 0, col, p->nnz);
   DG_CUDA(cp(val, p->val, 4 * p->nnz));
   DG_CUDA(cp(send_idx, p->send_idx, 4 * p->n_send));
   DG_CUDA(cp(rh_ptr, p->rh_ptr, 8 * (p->n_halo + 1)));
   DG_CUDA(cp(rh_col, p->rh_col, 4 * p->rh_nnz));
+  if (rh_col && p->rh_nnz > 0)
+    DG_LAUNCH(DIGEST_PROF_OTHER, s, 0, 0, k_clear_hot, dg::num_sms() * 4, 256, 0, rh_col,
+              p->rh_nnz);
   DG_CUDA(cp(rh_val, p->rh_val, 4 * p->rh_nnz));
   DG_CUDA(cudaStreamSynchronize(s));
   return DIGEST_OK;

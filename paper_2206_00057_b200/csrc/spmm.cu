@@ -96,11 +96,14 @@ __global__ void __launch_bounds__(256) k_spmm(SpmmArgs a) {
         const float* src[UNR];
         float vv[UNR];
         bool ok[UNR];
+        uint64_t pol[UNR];
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
           const int j = st * STEP + u * EG + g;
-          const int cj = __shfl_sync(0xffffffffu, c, j & 31);
+          const int cr = __shfl_sync(0xffffffffu, c, j & 31);
           const float x = __shfl_sync(0xffffffffu, v, j & 31);
+          const int cj = cr & 0x7fffffff;   // bit 31: L2-hot source row (partition hint)
+          pol[u] = cr < 0 ? pol_x : pol_s;
           ok[u] = g < EG && j < cnt;
           vv[u] = ok[u] ? x : 0.f;
           src[u] = (int64_t)cj < a.split ? a.X0 + (int64_t)cj * a.ld0
@@ -112,7 +115,7 @@ __global__ void __launch_bounds__(256) k_spmm(SpmmArgs a) {
 #pragma unroll
           for (int q = 0; q < VPL; ++q) {
             const int idx = cl + q * LC;
-            t[u][q] = (ok[u] && idx < w4) ? ld_gather(src[u] + 4 * idx, pol_x)
+            t[u][q] = (ok[u] && idx < w4) ? ld_gather(src[u] + 4 * idx, pol[u])
                                           : make_float4(0.f, 0.f, 0.f, 0.f);
           }
 #pragma unroll
@@ -178,6 +181,8 @@ __global__ void __launch_bounds__(256) k_spmm_rt(SpmmArgs a) {
   const int cl = lane % LC;
   const int g = lane / LC;
   const int w4 = a.width >> 2;
+  const uint64_t pol_x = policy_evict_last();
+  const uint64_t pol_s = policy_evict_first();
   int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t row = warp; row < a.n_rows; row += nwarps) {
@@ -199,11 +204,14 @@ __global__ void __launch_bounds__(256) k_spmm_rt(SpmmArgs a) {
         const float* src[UNR];
         float vv[UNR];
         bool ok[UNR];
+        bool hot[UNR];
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
           const int j = j0 + u * EG + g;
-          const int cj = __shfl_sync(0xffffffffu, c, j & 31);
+          const int cr = __shfl_sync(0xffffffffu, c, j & 31);
           const float x = __shfl_sync(0xffffffffu, v, j & 31);
+          const int cj = cr & 0x7fffffff;   // bit 31: L2-hot source row (partition hint)
+          hot[u] = cr < 0;
           ok[u] = g < EG && j < cnt;
           vv[u] = ok[u] ? x : 0.f;
           src[u] = (int64_t)cj < a.split ? a.X0 + (int64_t)cj * a.ld0
@@ -215,7 +223,9 @@ __global__ void __launch_bounds__(256) k_spmm_rt(SpmmArgs a) {
 #pragma unroll
           for (int q = 0; q < VPL; ++q) {
             const int idx = cl + q * LC;
-            t[u][q] = (ok[u] && idx < w4) ? ldg4(src[u] + 4 * idx) : make_float4(0.f, 0.f, 0.f, 0.f);
+            t[u][q] = !(ok[u] && idx < w4) ? make_float4(0.f, 0.f, 0.f, 0.f)
+                      : !a.hints ? ldg4(src[u] + 4 * idx)
+                                 : ld_gather(src[u] + 4 * idx, hot[u] ? pol_x : pol_s);
           }
 #pragma unroll
         for (int u = 0; u < UNR; ++u)

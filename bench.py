@@ -306,6 +306,10 @@ def run_ours(a, rank, world, local):
             "clocks": clocks,
             "spmm_gteps_rank0": gteps,
             "kernel_ms_per_step": {k: v["ms"] / a.steps for k, v in prof.items()},
+            # per (class, tag): spmm:<width>, gemm:1KKKKNNN forward-type, 2MMMMNNN weight grad,
+            # 3KKKKNNN CTA-pair forward-type
+            "kernel_detail_ms_per_step": {f"{d['cls']}:{d['tag']}": round(d["ms"] / a.steps, 3)
+                                          for d in detail},
             "setup_s": {"generate": t_gen, "partition_and_setup": t_part},
         }
         print(json.dumps(line), flush=True)

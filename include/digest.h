@@ -182,8 +182,10 @@ digest_status digest_store_destroy(digest_store* store);
  * order: AGG_FIRST computes A = P_m X_ext then Z = A W; XFORM_FIRST computes
  * T = X_ext W then Z = P_m T; AUTO picks AGG_FIRST iff d_in <= d_out (the SpMM runs
  * at width min(d_in, d_out)).  act RELU: H = max(Z, 0); NONE: H = Z (output layer).
- * `saved` (size from digest_layer_workspace) keeps what backward needs (A for
- * AGG_FIRST); the caller keeps X_local/X_halo and H_out alive until backward.
+ * `saved` (size from digest_layer_workspace) keeps what backward needs: A for
+ * AGG_FIRST and, for act RELU, the 1-bit activation mask 1[H > 0] (
+ * n_local rows of ld_words 32-bit words, bit j%32 of word j/32 = column j, words
+ * past (d_out+31)/32 are unspecified padding; see digest_layer_mask).  The caller keeps X_local/X_halo alive until backward.
  * scratch is per-call temporary memory. */
 typedef enum { DIGEST_ACT_NONE = 0, DIGEST_ACT_RELU = 1 } digest_act;
 typedef enum { DIGEST_ORDER_AUTO = 0, DIGEST_ORDER_AGG_FIRST = 1,
@@ -202,20 +204,30 @@ digest_status digest_layer_fwd(const digest_part* part, const float* X_local, in
                                int32_t d_in, int32_t d_out, int32_t act, int32_t order,
                                uint32_t flags, float* H_out, int64_t ld_h, void* saved,
                                void* scratch, void* stream);
-/* G_out: n_local x d_out gradient of the layer output (ld_g).  H_out: the forward
- * output (its sign is the ReLU mask, ReLU'(0) := 0); ignored for ACT_NONE.
- * flags DIGEST_BWD_G_IS_D: G_out already is D = G o sigma'(Z) (H_out unused).
+/* The 1-bit ReLU mask digest_layer_fwd (act RELU) left inside `saved`: *bits_h points
+ * into saved (device memory, caller-owned through saved), *ld_words_h words per row.
+ * Pass it as the next layer's backward gin_mask with DIGEST_BWD_GIN_MASK_BITS. */
+digest_status digest_layer_mask(const digest_part* part, int32_t d_in, int32_t d_out,
+                                int32_t order, const void* saved, const uint32_t** bits_h,
+                                int64_t* ld_words_h);
+/* G_out: n_local x d_out gradient of the layer output (ld_g).  sigma'(Z) for act RELU
+ * (ReLU'(0) := 0) is read from the 1-bit mask in `saved`; H_out (the forward output,
+ * its sign) is consulted only when saved is NULL (XFORM_FIRST); ignored for ACT_NONE.
+ * flags DIGEST_BWD_G_IS_D: G_out already is D = G o sigma'(Z).
  * G_W (d_in x d_out, overwritten) = (P_m X_ext)^T D with D = G_out o sigma'(Z).
  * G_in (n_local x d_in, ld_gi; NULL = skip, first layer) = P_in^T D W^T, multiplied
- * by 1[gin_mask > 0] when gin_mask != NULL -- pass the previous layer's output H to
- * emit that layer's D directly (fused ReLU', then call it with DIGEST_BWD_G_IS_D). */
-enum { DIGEST_BWD_G_IS_D = 1u };
+ * by the previous layer's ReLU' when gin_mask != NULL, which emits that layer's D
+ * directly (then call it with DIGEST_BWD_G_IS_D).  gin_mask is either a float
+ * n_local x d_in tensor (ld_gm floats; factor 1[gin_mask > 0], e.g. the previous H)
+ * or, with flags DIGEST_BWD_GIN_MASK_BITS, a 1-bit mask (ld_gm 32-bit words per row,
+ * e.g. digest_layer_mask of the previous layer). */
+enum { DIGEST_BWD_G_IS_D = 1u, DIGEST_BWD_GIN_MASK_BITS = 2u };
 digest_status digest_layer_bwd(const digest_part* part, const float* X_local, int64_t ld_x,
                                const float* X_halo, int64_t ld_xh, const float* W,
                                int32_t d_in, int32_t d_out, int32_t act, int32_t order,
                                const void* saved, const float* H_out, int64_t ld_h,
                                const float* G_out, int64_t ld_g, uint32_t flags, float* G_W,
-                               float* G_in, int64_t ld_gi, const float* gin_mask,
+                               float* G_in, int64_t ld_gi, const void* gin_mask,
                                int64_t ld_gm, float* G_halo, int64_t ld_gh, void* scratch,
                                void* stream);
 /* G_halo (n_halo x d_in, ld_gh; NULL = skip) = P_out^T D W^T: the gradient of this

@@ -70,6 +70,7 @@ _SIGS = {
                           _p], _i32),
     "digest_layer_bwd": ([_p, _p, _i64, _p, _i64, _p, _i32, _i32, _i32, _i32, _p, _p, _i64, _p, _i64,
                           _u32, _p, _p, _i64, _p, _i64, _p, _i64, _p, _p], _i32),
+    "digest_layer_mask": ([_p, _i32, _i32, _i32, _p, _p, _p], _i32),
     "digest_store_grad_buffer": ([_p, _i32, _p, _p], _i32),
     "digest_return_halo_grad": ([_p, _i32, _p, _i64, _p, _i64, _p], _i32),
     "digest_propagate": ([_p, _i32, _p, _i64, _p, _i64, _i32, _p, _i64, _p], _i32),
@@ -256,21 +257,35 @@ def digest_layer_fwd(part, X_local, X_halo, ld_xh, W, d_in, d_out, act, order, H
                                 ptr(saved), ptr(scratch), stream_ptr(stream)))
 
 
+def digest_layer_mask(part, d_in, d_out, order, saved):
+    """(device address, words per row) of the 1-bit ReLU mask inside `saved`."""
+    p, ld = C.c_void_p(), C.c_int64()
+    _check(lib.digest_layer_mask(part, d_in, d_out, order, ptr(saved), C.byref(p), C.byref(ld)))
+    return p.value, ld.value
+
+
 BWD_G_IS_D = 1
+BWD_GIN_MASK_BITS = 2
 
 
 def digest_layer_bwd(part, X_local, X_halo, ld_xh, W, d_in, d_out, act, order, saved, H_out,
                      G_out, G_W, G_in, scratch, stream=None, flags=0, gin_mask=None,
                      G_halo=None, ld_gh=0):
-    """G_halo may be a tensor or a raw device address (the store's gradient buffer)."""
+    """G_halo may be a tensor or a raw device address (the store's gradient buffer).
+    gin_mask: a float tensor, or (address, words per row) of a 1-bit mask
+    (digest_layer_mask), which sets BWD_GIN_MASK_BITS."""
     if isinstance(G_halo, torch.Tensor):
         ld_gh = ld_of(G_halo)
+    if isinstance(gin_mask, tuple):
+        gm, ld_gm = gin_mask
+        flags |= BWD_GIN_MASK_BITS
+    else:
+        gm, ld_gm = ptr(gin_mask), ld_of(gin_mask) if gin_mask is not None else 0
     _check(lib.digest_layer_bwd(part, ptr(X_local), ld_of(X_local), ptr(X_halo), ld_xh, ptr(W),
                                 d_in, d_out, act, order, ptr(saved), ptr(H_out),
                                 ld_of(H_out) if H_out is not None else 0, ptr(G_out),
                                 ld_of(G_out), flags, ptr(G_W), ptr(G_in),
-                                ld_of(G_in) if G_in is not None else 0, ptr(gin_mask),
-                                ld_of(gin_mask) if gin_mask is not None else 0, ptr(G_halo),
+                                ld_of(G_in) if G_in is not None else 0, gm, ld_gm, ptr(G_halo),
                                 ld_gh, ptr(scratch), stream_ptr(stream)))
 
 

@@ -77,6 +77,7 @@ k_gemm(GemmArgs g, int64_t k_per_split, float* partial) {
       } else {
         if (g.relu) v = fmaxf(v, 0.f);
         if (g.mask && !(g.mask[gi * g.ldm + gj] > 0.f)) v = 0.f;
+        if (g.mbits && !mask_bit(g.mbits, g.ldmb, gi, gj)) v = 0.f;
         g.C[gi * g.ldc + gj] = v;
       }
     }
@@ -111,6 +112,40 @@ __global__ void k_relu_mask(const float* __restrict__ G, int64_t ldg, const floa
   }
 }
 
+__global__ void k_relu_mask_bits(const float* __restrict__ G, int64_t ldg,
+                                 const uint32_t* __restrict__ mb, int64_t ldmb,
+                                 float* __restrict__ D, int64_t ldd, int64_t n, int w4) {
+  int64_t total = n * w4;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = t / w4;
+    int c = (int)(t % w4);
+    float4 g = reinterpret_cast<const float4*>(G + i * ldg)[c];
+    const uint32_t m = __ldg(mb + i * ldmb + (c >> 3)) >> ((c & 7) * 4);
+    g.x = (m & 1u) ? g.x : 0.f;
+    g.y = (m & 2u) ? g.y : 0.f;
+    g.z = (m & 4u) ? g.z : 0.f;
+    g.w = (m & 8u) ? g.w : 0.f;
+    reinterpret_cast<float4*>(D + i * ldd)[c] = g;
+  }
+}
+
+// one warp per (row, word): lane j tests column 32*word + j
+__global__ void k_sign_bits(const float* __restrict__ C, int64_t ldc, int64_t n, int w,
+                            int nw, uint32_t* __restrict__ bits, int64_t ldb) {
+  const int lane = threadIdx.x & 31;
+  const int64_t total = n * nw;
+  for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < total;
+       t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t i = t / nw;
+    const int k = (int)(t % nw);
+    const int j = 32 * k + lane;
+    const bool pos = j < w && C[i * ldc + j] > 0.f;
+    const uint32_t word = __ballot_sync(0xffffffffu, pos);
+    if (lane == 0) bits[i * ldb + k] = word;
+  }
+}
+
 constexpr int64_t kWgradRowsPerSplit = 2048;
 
 int64_t wgrad_splits(int64_t K) {
@@ -133,11 +168,16 @@ digest_status gemm_simt(const GemmArgs& g, cudaStream_t s) {
     GemmArgs sub = g;
     sub.A = g.A + t0 * BM * g.sAi;
     sub.C = g.C + t0 * BM * g.ldc;
+    if (g.mask) sub.mask = g.mask + t0 * BM * g.ldm;
+    if (g.mbits) sub.mbits = g.mbits + t0 * BM * g.ldmb;
     sub.M = min(g.M - t0 * BM, (int64_t)65535 * BM);
     dim3 gr((unsigned)ceil_div(g.N, BN), (unsigned)ceil_div(sub.M, BM), 1);
     DG_LAUNCH(DIGEST_PROF_GEMM, s, bytes * sub.M / g.M, flops * sub.M / g.M, k_gemm, gr,
               kThreads, 0, sub, g.K, (float*)nullptr);
   }
+  // the 1-bit output mask: a second pass over C (this kernel only serves small or
+  // oddly strided products; the tensor-core epilogue writes the bits in place)
+  if (g.obits) DG_TRY(sign_bits(g.C, g.ldc, g.M, g.N, g.obits, g.ldob, s));
   return DIGEST_OK;
 }
 
@@ -211,6 +251,27 @@ digest_status relu_mask(const float* G, int64_t ldg, const float* H, int64_t ldh
   int64_t blocks = min(ceil_div(total, 256), (int64_t)num_sms() * 16);
   DG_LAUNCH(DIGEST_PROF_OTHER, s, 12.0 * total * 4, 0, k_relu_mask, (unsigned)blocks, 256, 0, G,
             ldg, H, ldh, D, ldd, n, w4);
+  return DIGEST_OK;
+}
+
+digest_status relu_mask_bits(const float* G, int64_t ldg, const uint32_t* mbits, int64_t ldmb,
+                             float* D, int64_t ldd, int64_t n, int32_t w, cudaStream_t s) {
+  if (n == 0) return DIGEST_OK;
+  int w4 = w / 4;
+  int64_t total = n * w4;
+  int64_t blocks = min(ceil_div(total, 256), (int64_t)num_sms() * 16);
+  DG_LAUNCH(DIGEST_PROF_OTHER, s, 8.0 * total * 4 + (double)n * ((w + 31) / 32) * 4, 0,
+            k_relu_mask_bits, (unsigned)blocks, 256, 0, G, ldg, mbits, ldmb, D, ldd, n, w4);
+  return DIGEST_OK;
+}
+
+digest_status sign_bits(const float* C, int64_t ldc, int64_t n, int32_t w, uint32_t* bits,
+                        int64_t ldb, cudaStream_t s) {
+  if (n == 0 || w == 0) return DIGEST_OK;
+  const int nw = (w + 31) / 32;
+  int64_t blocks = min(ceil_div(n * nw * 32, 256), (int64_t)num_sms() * 16);
+  DG_LAUNCH(DIGEST_PROF_OTHER, s, 4.0 * n * w + 4.0 * n * nw, 0, k_sign_bits, (unsigned)blocks,
+            256, 0, C, ldc, n, w, nw, bits, ldb);
   return DIGEST_OK;
 }
 

@@ -18,6 +18,7 @@
 
 #include <mutex>
 
+#include "gemm_epi.cuh"
 #include "kernels.cuh"
 #include "tc_util.cuh"
 
@@ -71,9 +72,10 @@ struct Cfg {
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
 k_gemm_tf32x3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBh,
-              const __grid_constant__ CUtensorMap tmBl, float* __restrict__ C, int64_t ldc,
-              int64_t M, int N, int K, int relu, const float* __restrict__ mask, int64_t ldm) {
+              const __grid_constant__ CUtensorMap tmBl, const EpiArgs e, int K) {
   using G = Cfg<BN>;
+  const int64_t M = e.M;
+  const int N = e.N;
   constexpr int S = G::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -196,53 +198,14 @@ k_gemm_tf32x3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     const int q = warp & 3;   // TMEM lane quarter this warp may access
     int acc = 0;
     uint32_t aph = 0;
-    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-      const int64_t m0 = (t / n_tiles_n) * kBM;
-      const int n0 = (int)((t % n_tiles_n) * BN);
+    float4* stg = reinterpret_cast<float4*>(epi + q * 4096);
+    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {   // n_tiles_n == 1 (BN >= N)
+      const int64_t m0 = t * kBM;
+      const int64_t tn = t + gridDim.x;
+      epi_prefetch_next<BN>(e, tn < n_tiles ? tn * kBM : -1, threadIdx.x % 128);
       tc::mbar_wait(&tfull[acc], aph);
       tc::tc_fence_after();
-      // TMEM gives lane l the 32 columns of row l; stage them through a per-warp
-      // 32 x 128 B shared buffer (16 B chunks XOR-swizzled by row, conflict-free) so
-      // the global stores are full 128 B lines: 4 rows x 8 chunks per warp store.
-      float4* stg = reinterpret_cast<float4*>(epi + q * 4096);
-#pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        uint32_t r[32];
-        tc::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * G::ACC + c0, r);
-        tc::tmem_ld_wait();
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          float4 v = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
-                                 __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
-          if (relu) {
-            v.x = fmaxf(v.x, 0.f);
-            v.y = fmaxf(v.y, 0.f);
-            v.z = fmaxf(v.z, 0.f);
-            v.w = fmaxf(v.w, 0.f);
-          }
-          stg[lane * 8 + (j ^ (lane & 7))] = v;
-        }
-        __syncwarp();
-        const int ch = lane & 7;
-#pragma unroll
-        for (int it = 0; it < 8; ++it) {
-          const int rr = it * 4 + (lane >> 3);
-          const int64_t row = m0 + q * 32 + rr;
-          const int col = n0 + c0 + 4 * ch;
-          if (row < M && col < N) {
-            float4 v = stg[rr * 8 + (ch ^ (rr & 7))];
-            if (mask) {
-              const float4 mk = __ldg(reinterpret_cast<const float4*>(mask + row * ldm + col));
-              v.x = mk.x > 0.f ? v.x : 0.f;
-              v.y = mk.y > 0.f ? v.y : 0.f;
-              v.z = mk.z > 0.f ? v.z : 0.f;
-              v.w = mk.w > 0.f ? v.w : 0.f;
-            }
-            *reinterpret_cast<float4*>(C + row * ldc + col) = v;
-          }
-        }
-        __syncwarp();
-      }
+      epi_tile<BN>(e, tmem_base + acc * G::ACC, stg, m0, q, lane);
       tc::tc_fence_before();
       tc::mbar_arrive(&tempty[acc]);
       acc ^= 1;
@@ -307,12 +270,18 @@ digest_status launch_tc(const GemmArgs& g, const CUtensorMap& tA, const CUtensor
   const int64_t grid = tiles < num_sms() ? tiles : num_sms();
   const double flops = 2.0 * (double)g.M * g.N * g.K;
   const double bytes = 4.0 * ((double)g.M * g.K + (double)g.M * g.N + 2.0 * g.N * g.K);
-  DG_LAUNCH(DIGEST_PROF_GEMM, s, bytes, flops, k_gemm_tf32x3<BN>, (unsigned)grid, kThreads,
-            G::SMEM, tA, tBh, tBl, g.C, g.ldc, g.M, g.N, (int)g.K, g.relu, g.mask, g.ldm);
+  // profile tag: 1KKKKNNN (forward-type GEMM, K and N)
+  DG_LAUNCH_TAG(DIGEST_PROF_GEMM, 10000000 + (int)g.K * 1000 + g.N, s, bytes, flops,
+                k_gemm_tf32x3<BN>, (unsigned)grid, kThreads, G::SMEM, tA, tBh, tBl, epi_of(g),
+                (int)g.K);
   return DIGEST_OK;
 }
 
 }  // namespace
+
+bool gemm_tc2_enabled(int N);
+digest_status gemm_tc2(const GemmArgs& g, const float* hi, const float* lo, int Kp,
+                       cudaStream_t s);
 
 bool gemm_tc_eligible(const GemmArgs& g) {
   static int force_simt = -1;
@@ -326,6 +295,7 @@ bool gemm_tc_eligible(const GemmArgs& g) {
   if (g.N % 4 != 0 || g.N > 256 || g.K < 8 || g.K > (1 << 20)) return false;
   if (g.ldc % 4 != 0 || ((uintptr_t)g.C & 15) != 0) return false;
   if (g.mask && (g.ldm % 4 != 0 || ((uintptr_t)g.mask & 15) != 0)) return false;
+  if (g.mask && g.obits) return false;   // the epilogue's bits precede the float-mask stage
   if (g.M < 256) return false;   // tiny problems: the CUDA-core kernel launches cheaper
   return true;
 }
@@ -343,6 +313,7 @@ digest_status gemm_tc(const GemmArgs& g, cudaStream_t s) {
     DG_LAUNCH(DIGEST_PROF_OTHER, s, 12.0 * total, 0, k_prep_b, (unsigned)blocks, 256, 0, g.B,
               g.sBk, g.sBj, K, N, Kp, hi, lo);
   }
+  if (gemm_tc2_enabled(N) && g.M >= 2 * kBM) return gemm_tc2(g, hi, lo, Kp, s);
   int BN = N <= 16 ? 16 : N <= 32 ? 32 : N <= 48 ? 48 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
   CUtensorMap tA, tBh, tBl;
   bool ok = make_tmap_2d(&tA, g.A, (uint64_t)K, (uint64_t)g.M, (uint64_t)g.sAi * 4, kBK, kBM) &&

@@ -26,8 +26,16 @@ struct SpmmArgs {
   int32_t relu;
   const float* mask;   // optional: Y *= 1[mask > 0] (fused ReLU' of the consumer layer)
   int64_t ldm;
+  const uint32_t* mbits;   // optional: Y *= bit(mbits, row, col) (the 1-bit form of `mask`)
+  int64_t ldmb;            // words per mbits row
+  uint32_t* obits;         // optional: write bit(obits, row, col) = Y[row, col] > 0
+  int64_t ldob;
   int32_t hints;       // L2 evict_last on gathers / evict_first on CSR streams
 };
+// 1-bit activation masks: bit (col & 31) of word row * ld + (col >> 5).
+__device__ __forceinline__ bool mask_bit(const uint32_t* bits, int64_t ld, int64_t row, int col) {
+  return (__ldg(bits + row * ld + (col >> 5)) >> (col & 31)) & 1u;
+}
 digest_status spmm(const SpmmArgs& a, cudaStream_t s);
 
 // C = A * B (+ optional ReLU) with generic strides:
@@ -45,6 +53,10 @@ struct GemmArgs {
   int32_t relu;
   const float* mask;   // optional: C *= 1[mask > 0] (fused ReLU' of the consumer layer)
   int64_t ldm;
+  const uint32_t* mbits;   // optional: C *= bit(mbits, i, j)
+  int64_t ldmb;
+  uint32_t* obits;         // optional: bit(obits, i, j) = C[i, j] > 0
+  int64_t ldob;
 };
 digest_status gemm(const GemmArgs& g, cudaStream_t s);        // dispatch (tensor core if eligible)
 digest_status gemm_simt(const GemmArgs& g, cudaStream_t s);   // CUDA-core fp32
@@ -73,5 +85,11 @@ digest_status wgrad_simt(const WgradSeg* segs, int nseg, int32_t M, int32_t N, f
 // D = G o 1[H > 0] (n x w)
 digest_status relu_mask(const float* G, int64_t ldg, const float* H, int64_t ldh, float* D,
                         int64_t ldd, int64_t n, int32_t w, cudaStream_t s);
+// D = G o bit(mbits) (n x w)
+digest_status relu_mask_bits(const float* G, int64_t ldg, const uint32_t* mbits, int64_t ldmb,
+                             float* D, int64_t ldd, int64_t n, int32_t w, cudaStream_t s);
+// bits(i, j) = C[i, j] > 0 for j < w; the pad bits of each row's last word are 0
+digest_status sign_bits(const float* C, int64_t ldc, int64_t n, int32_t w, uint32_t* bits,
+                        int64_t ldb, cudaStream_t s);
 
 }  // namespace dg

@@ -33,6 +33,8 @@ struct Plan {
   bool agg_first;
   int64_t n, h;
   int64_t ldi, ldo;   // padded widths of d_in / d_out scratch rows
+  int64_t ldmb;       // 32-bit words per row of the 1-bit ReLU mask (multiple of 4)
+  size_t bits_off;    // byte offset of the mask inside `saved`
   size_t saved, scratch;
 };
 
@@ -50,6 +52,7 @@ digest_status make_plan(const digest_part* p, int32_t d_in, int32_t d_out, int32
   pl->ldo = round_up(d_out, 4);
   const size_t f = sizeof(float);
   size_t wg = dg::wgrad_scratch_bytes(pl->n + pl->h, d_in, d_out);
+  pl->ldmb = round_up((d_out + 31) / 32, 4);
   if (pl->agg_first) {
     pl->saved = f * pl->n * pl->ldi;
     size_t bwd = f * pl->n * pl->ldo + f * pl->n * pl->ldi + wg;
@@ -60,6 +63,9 @@ digest_status make_plan(const digest_part* p, int32_t d_in, int32_t d_out, int32
     size_t bwd = f * pl->n * pl->ldo + f * (pl->n + pl->h) * pl->ldo + wg;
     pl->scratch = fwd > bwd ? fwd : bwd;
   }
+  // saved = [A (AGG_FIRST) | 1-bit ReLU mask of H, n x ldmb words]
+  pl->bits_off = round_up(pl->saved, 256);
+  pl->saved = pl->bits_off + sizeof(uint32_t) * pl->n * pl->ldmb;
   pl->saved = round_up(pl->saved, 256);
   pl->scratch = round_up(pl->scratch, 256);
   return DIGEST_OK;
@@ -176,15 +182,22 @@ digest_status digest_layer_fwd(const digest_part* p, const float* X_local, int64
   if (pl.h > 0) DG_TRY(check_mat(X_halo, ld_xh, d_in, "X_halo"));
   DG_TRY(check_mat(H_out, ld_h, d_out, "H_out"));
   DG_ARG(W, DIGEST_E_INVALID, "W is NULL");
-  DG_ARG(pl.saved == 0 || saved, DIGEST_E_INVALID, "saved is NULL");
+  const int relu = act == DIGEST_ACT_RELU;
+  DG_ARG(saved || !(pl.agg_first || relu), DIGEST_E_INVALID, "saved is NULL");
   DG_ARG(pl.agg_first || scratch, DIGEST_E_INVALID, "scratch is NULL");
   cudaStream_t s = dg::as_stream(stream);
-  const int relu = act == DIGEST_ACT_RELU;
+  // ReLU layers also emit the 1-bit mask 1[H > 0] into saved: the
+  // backward's sigma' reads 1/32 of the bytes of H.
+  uint32_t* bits = relu ? reinterpret_cast<uint32_t*>(static_cast<char*>(saved) + pl.bits_off)
+                        : nullptr;
   if (pl.agg_first) {
     float* A = reinterpret_cast<float*>(saved);
     if (!reuse)   // A = P_m X_ext; with REUSE_SAVED the caller's static inputs were aggregated before
       DG_TRY(dg::spmm(spmm_full(p, X_local, ld_x, X_halo, ld_xh, A, pl.ldi, d_in, 0), s));
-    DG_TRY(dg::gemm(gemm_rm(A, pl.ldi, W, d_out, H_out, ld_h, pl.n, d_out, d_in, relu), s));
+    dg::GemmArgs g = gemm_rm(A, pl.ldi, W, d_out, H_out, ld_h, pl.n, d_out, d_in, relu);
+    g.obits = bits;
+    g.ldob = pl.ldmb;
+    DG_TRY(dg::gemm(g, s));
   } else {
     size_t off = 0;
     float* T = carve(scratch, off, sizeof(float) * (pl.n + pl.h) * pl.ldo);
@@ -192,9 +205,22 @@ digest_status digest_layer_fwd(const digest_part* p, const float* X_local, int64
     if (pl.h > 0)
       DG_TRY(dg::gemm(gemm_rm(X_halo, ld_xh, W, d_out, T + pl.n * pl.ldo, pl.ldo, pl.h, d_out,
                               d_in, 0), s));
-    DG_TRY(dg::spmm(spmm_full(p, T, pl.ldo, T + pl.n * pl.ldo, pl.ldo, H_out, ld_h, d_out, relu),
-                    s));
+    dg::SpmmArgs a = spmm_full(p, T, pl.ldo, T + pl.n * pl.ldo, pl.ldo, H_out, ld_h, d_out, relu);
+    a.obits = bits;
+    a.ldob = pl.ldmb;
+    DG_TRY(dg::spmm(a, s));
   }
+  return DIGEST_OK;
+}
+
+digest_status digest_layer_mask(const digest_part* p, int32_t d_in, int32_t d_out, int32_t order,
+                                const void* saved, const uint32_t** bits_h,
+                                int64_t* ld_words_h) {
+  Plan pl;
+  DG_TRY(make_plan(p, d_in, d_out, order, &pl));
+  DG_ARG(saved && bits_h && ld_words_h, DIGEST_E_INVALID, "NULL argument");
+  *bits_h = reinterpret_cast<const uint32_t*>(static_cast<const char*>(saved) + pl.bits_off);
+  *ld_words_h = pl.ldmb;
   return DIGEST_OK;
 }
 
@@ -203,16 +229,25 @@ digest_status digest_layer_bwd(const digest_part* p, const float* X_local, int64
                                int32_t d_out, int32_t act, int32_t order, const void* saved,
                                const float* H_out, int64_t ld_h, const float* G_out, int64_t ld_g,
                                uint32_t flags, float* G_W, float* G_in, int64_t ld_gi,
-                               const float* gin_mask, int64_t ld_gm, float* G_halo,
+                               const void* gin_mask, int64_t ld_gm, float* G_halo,
                                int64_t ld_gh, void* scratch, void* stream) {
   Plan pl;
   DG_TRY(make_plan(p, d_in, d_out, order, &pl));
   DG_ARG(act == DIGEST_ACT_NONE || act == DIGEST_ACT_RELU, DIGEST_E_INVALID, "bad act");
   DG_TRY(check_mat(G_out, ld_g, d_out, "G_out"));
   const bool g_is_d = (flags & DIGEST_BWD_G_IS_D) != 0;
-  if (act == DIGEST_ACT_RELU && !g_is_d) DG_TRY(check_mat(H_out, ld_h, d_out, "H_out"));
+  const bool gm_bits = (flags & DIGEST_BWD_GIN_MASK_BITS) != 0;
+  // sigma' of this layer: the 1-bit mask the forward left in saved; H_out only if
+  // saved is NULL (transform-first layers may be called without it)
+  const bool d_from_bits = act == DIGEST_ACT_RELU && !g_is_d && saved != nullptr;
+  if (act == DIGEST_ACT_RELU && !g_is_d && !saved) DG_TRY(check_mat(H_out, ld_h, d_out, "H_out"));
   if (G_in) DG_TRY(check_mat(G_in, ld_gi, d_in, "G_in"));
-  if (G_in && gin_mask) DG_TRY(check_mat(gin_mask, ld_gm, d_in, "gin_mask"));
+  if (G_in && gin_mask && !gm_bits) DG_TRY(check_mat(gin_mask, ld_gm, d_in, "gin_mask"));
+  if (G_in && gin_mask && gm_bits)
+    DG_ARG(ld_gm >= (d_in + 31) / 32, DIGEST_E_INVALID, "gin_mask (bits): ld %lld words < %d",
+           (long long)ld_gm, (d_in + 31) / 32);
+  const float* gm_f = gm_bits ? nullptr : static_cast<const float*>(gin_mask);
+  const uint32_t* gm_b = gm_bits ? static_cast<const uint32_t*>(gin_mask) : nullptr;
   if (G_halo && pl.h > 0) DG_TRY(check_mat(G_halo, ld_gh, d_in, "G_halo"));
   const bool want_halo = G_halo && pl.h > 0;
   DG_ARG(W && G_W && scratch, DIGEST_E_INVALID, "W, G_W and scratch must be non-NULL");
@@ -225,7 +260,13 @@ digest_status digest_layer_bwd(const digest_part* p, const float* X_local, int64
   int64_t ldd = ld_g;
   if (act == DIGEST_ACT_RELU && !g_is_d) {
     float* Dm = carve(scratch, off, sizeof(float) * pl.n * pl.ldo);
-    DG_TRY(dg::relu_mask(G_out, ld_g, H_out, ld_h, Dm, pl.ldo, pl.n, d_out, s));
+    if (d_from_bits)
+      DG_TRY(dg::relu_mask_bits(G_out, ld_g,
+                                reinterpret_cast<const uint32_t*>(
+                                    static_cast<const char*>(saved) + pl.bits_off),
+                                pl.ldmb, Dm, pl.ldo, pl.n, d_out, s));
+    else
+      DG_TRY(dg::relu_mask(G_out, ld_g, H_out, ld_h, Dm, pl.ldo, pl.n, d_out, s));
     D = Dm;
     ldd = pl.ldo;
   } else {
@@ -247,8 +288,10 @@ digest_status digest_layer_bwd(const digest_part* p, const float* X_local, int64
     }
     if (G_in) {
       dg::SpmmArgs a = spmm_in(p, U, pl.ldi, G_in, ld_gi, d_in);
-      a.mask = gin_mask;
+      a.mask = gm_f;
       a.ldm = ld_gm;
+      a.mbits = gm_b;
+      a.ldmb = ld_gm;
       DG_TRY(dg::spmm(a, s));
     }
     if (want_halo)   // P:816 term for the owners of the halo rows: G_halo = P_out^T U
@@ -268,8 +311,10 @@ digest_status digest_layer_bwd(const digest_part* p, const float* X_local, int64
       dg::GemmArgs g = gemm_rm(S, pl.ldo, W, d_out, G_in, ld_gi, pl.n, d_in, d_out, 0);
       g.sBk = 1;
       g.sBj = d_out;
-      g.mask = gin_mask;
+      g.mask = gm_f;
       g.ldm = ld_gm;
+      g.mbits = gm_b;
+      g.ldmb = ld_gm;
       DG_TRY(dg::gemm(g, s));
     }
     if (want_halo) {   // P:816 term for the owners of the halo rows: G_halo = S_halo W^T

@@ -49,6 +49,64 @@ __device__ __forceinline__ float4 ldg4(const float* p) {
   return __ldg(reinterpret_cast<const float4*>(p));
 }
 
+// Row epilogue shared by both kernels.  Lanes of edge group 0 hold the reduced row
+// (float4 column idx = cl + q*LC): optional ReLU, the consumer's ReLU' (float mask or
+// 1-bit mask), the store, and optionally the 1-bit mask of the stored row (SURVEY §8
+// a5): word k collects the nibbles of float4 columns 8k..8k+7 with a warp OR-reduce.
+template <int LC, int VPL>
+__device__ __forceinline__ void spmm_row_epilogue(const SpmmArgs& a, int64_t row, int lane, int cl,
+                                                  int g, int w4, float4 (&acc)[VPL]) {
+  uint32_t nib[VPL];
+#pragma unroll
+  for (int q = 0; q < VPL; ++q) nib[q] = 0;
+  if (g == 0) {
+    float* y = a.Y + row * a.ldy;
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) {
+      const int idx = cl + q * LC;
+      if (idx < w4) {
+        float4 r = acc[q];
+        if (a.relu) {
+          r.x = fmaxf(r.x, 0.f);
+          r.y = fmaxf(r.y, 0.f);
+          r.z = fmaxf(r.z, 0.f);
+          r.w = fmaxf(r.w, 0.f);
+        }
+        if (a.mask) {
+          const float4 mk = ldg4(a.mask + row * a.ldm + 4 * idx);
+          r.x = mk.x > 0.f ? r.x : 0.f;
+          r.y = mk.y > 0.f ? r.y : 0.f;
+          r.z = mk.z > 0.f ? r.z : 0.f;
+          r.w = mk.w > 0.f ? r.w : 0.f;
+        }
+        if (a.mbits) {
+          const uint32_t m = __ldg(a.mbits + row * a.ldmb + (idx >> 3)) >> ((idx & 7) * 4);
+          r.x = (m & 1u) ? r.x : 0.f;
+          r.y = (m & 2u) ? r.y : 0.f;
+          r.z = (m & 4u) ? r.z : 0.f;
+          r.w = (m & 8u) ? r.w : 0.f;
+        }
+        nib[q] = (r.x > 0.f ? 1u : 0u) | (r.y > 0.f ? 2u : 0u) | (r.z > 0.f ? 4u : 0u) |
+                 (r.w > 0.f ? 8u : 0u);
+        reinterpret_cast<float4*>(y)[idx] = r;
+      }
+    }
+  }
+  if (a.obits) {   // warp-uniform
+    const int nw = (w4 + 7) >> 3;
+    for (int k = 0; k < nw; ++k) {
+      uint32_t c = 0;
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) {
+        const int idx = cl + q * LC;
+        if ((idx >> 3) == k) c |= nib[q] << ((idx & 7) * 4);
+      }
+      c = __reduce_or_sync(0xffffffffu, c);
+      if (lane == 0) a.obits[row * a.ldob + k] = c;
+    }
+  }
+}
+
 // One warp per output row.  The warp is split into EG = 32/LC edge groups of LC
 // lanes; edge group g handles edges j = g, g+EG, ... of the row, lane c of a group
 // owns float4 columns c, c+LC, ... (VPL of them).  The 32 (col, val) pairs of a
@@ -69,6 +127,9 @@ __global__ void __launch_bounds__(256) k_spmm(SpmmArgs a) {
   const int w4 = a.width >> 2;
   const uint64_t pol_x = a.hints ? policy_evict_last() : policy_evict_normal();
   const uint64_t pol_s = a.hints ? policy_evict_first() : policy_evict_normal();
+  const uint64_t pol_c = a.hints == 1   ? policy_evict_first()
+                         : a.hints == 3 ? policy_evict_last()
+                                        : policy_evict_normal();
   int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t row = warp; row < a.n_rows; row += nwarps) {
@@ -103,7 +164,7 @@ __global__ void __launch_bounds__(256) k_spmm(SpmmArgs a) {
           const int cr = __shfl_sync(0xffffffffu, c, j & 31);
           const float x = __shfl_sync(0xffffffffu, v, j & 31);
           const int cj = cr & 0x7fffffff;   // bit 31: L2-hot source row (partition hint)
-          pol[u] = cr < 0 ? pol_x : pol_s;
+          pol[u] = cr < 0 ? pol_x : pol_c;
           ok[u] = g < EG && j < cnt;
           vv[u] = ok[u] ? x : 0.f;
           src[u] = (int64_t)cj < a.split ? a.X0 + (int64_t)cj * a.ld0
@@ -145,30 +206,7 @@ __global__ void __launch_bounds__(256) k_spmm(SpmmArgs a) {
           acc[q].w += w;
         }
       }
-    if (g == 0) {
-      float* y = a.Y + row * a.ldy;
-#pragma unroll
-      for (int q = 0; q < VPL; ++q) {
-        const int idx = cl + q * LC;
-        if (idx < w4) {
-          float4 r = acc[q];
-          if (a.relu) {
-            r.x = fmaxf(r.x, 0.f);
-            r.y = fmaxf(r.y, 0.f);
-            r.z = fmaxf(r.z, 0.f);
-            r.w = fmaxf(r.w, 0.f);
-          }
-          if (a.mask) {
-            const float4 mk = ldg4(a.mask + row * a.ldm + 4 * idx);
-            r.x = mk.x > 0.f ? r.x : 0.f;
-            r.y = mk.y > 0.f ? r.y : 0.f;
-            r.z = mk.z > 0.f ? r.z : 0.f;
-            r.w = mk.w > 0.f ? r.w : 0.f;
-          }
-          reinterpret_cast<float4*>(y)[idx] = r;
-        }
-      }
-    }
+    spmm_row_epilogue<LC, VPL>(a, row, lane, cl, g, w4, acc);
   }
 }
 
@@ -182,7 +220,9 @@ __global__ void __launch_bounds__(256) k_spmm_rt(SpmmArgs a) {
   const int g = lane / LC;
   const int w4 = a.width >> 2;
   const uint64_t pol_x = policy_evict_last();
-  const uint64_t pol_s = policy_evict_first();
+  const uint64_t pol_s = a.hints == 1   ? policy_evict_first()
+                         : a.hints == 3 ? policy_evict_last()
+                                        : policy_evict_normal();
   int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t row = warp; row < a.n_rows; row += nwarps) {
@@ -254,30 +294,7 @@ __global__ void __launch_bounds__(256) k_spmm_rt(SpmmArgs a) {
           acc[q].w += w;
         }
       }
-    if (g == 0) {
-      float* y = a.Y + row * a.ldy;
-#pragma unroll
-      for (int q = 0; q < VPL; ++q) {
-        const int idx = cl + q * LC;
-        if (idx < w4) {
-          float4 r = acc[q];
-          if (a.relu) {
-            r.x = fmaxf(r.x, 0.f);
-            r.y = fmaxf(r.y, 0.f);
-            r.z = fmaxf(r.z, 0.f);
-            r.w = fmaxf(r.w, 0.f);
-          }
-          if (a.mask) {
-            const float4 mk = ldg4(a.mask + row * a.ldm + 4 * idx);
-            r.x = mk.x > 0.f ? r.x : 0.f;
-            r.y = mk.y > 0.f ? r.y : 0.f;
-            r.z = mk.z > 0.f ? r.z : 0.f;
-            r.w = mk.w > 0.f ? r.w : 0.f;
-          }
-          reinterpret_cast<float4*>(y)[idx] = r;
-        }
-      }
-    }
+    spmm_row_epilogue<LC, VPL>(a, row, lane, cl, g, w4, acc);
   }
 }
 
@@ -330,7 +347,7 @@ digest_status spmm(const SpmmArgs& a0, cudaStream_t s) {
   DG_ARG(a.width > 0 && a.width % 4 == 0, DIGEST_E_INVALID,
          "SpMM width %d must be a positive multiple of 4", a.width);
   const int slab = spmm_slab_width(a);
-  if (slab <= 0 || slab % 4 != 0 || slab >= a.width) return spmm_one(a, s);
+  if (slab <= 0 || slab % 4 != 0 || slab >= a.width || a.mbits || a.obits) return spmm_one(a, s);
   for (int c0 = 0; c0 < a.width; c0 += slab) {
     SpmmArgs b = a;
     b.X0 = a.X0 + c0;

@@ -335,8 +335,10 @@ digest_status launch_seg(const WgradSeg& sg, int M, int N, int grid_x, float* pa
   dim3 grid((unsigned)grid_x, (unsigned)ytiles);
   const double flops = 2.0 * (double)M * N * sg.K;
   const double bytes = 4.0 * (double)sg.K * (M + N);
-  DG_LAUNCH(DIGEST_PROF_GEMM, s, bytes, flops, (k_wgrad_bf16x6<MT, BN>), grid, kThreads, G::SMEM,
-            tA, tB, sg.K, kpc, M, N, partial, wgrad_dbg());
+  // profile tag: 2MMMMNNN (weight gradient, M = d_in, N = d_out)
+  DG_LAUNCH_TAG(DIGEST_PROF_GEMM, 20000000 + M * 1000 + N, s, bytes, flops,
+                (k_wgrad_bf16x6<MT, BN>), grid, kThreads, G::SMEM, tA, tB, sg.K, kpc, M, N,
+                partial, wgrad_dbg());
   return DIGEST_OK;
 }
 

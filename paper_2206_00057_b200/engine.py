@@ -108,6 +108,10 @@ class DigestWorker:
             self.saved.append(torch.empty(max(sv, 256), dtype=torch.uint8, device=dev))
             scratch = max(scratch, sc)
         self.scratch = torch.empty(max(scratch, 256), dtype=torch.uint8, device=dev)
+        # 1-bit ReLU masks the forward writes into saved
+        self.mask_bits = [None] + [
+            D.digest_layer_mask(part.handle, dims[l - 1], dims[l], self.layer_order(l),
+                                self.saved[l]) for l in range(1, self.L + 1)]
         self.G = [None] + [torch.empty(n, dims[l], device=dev) for l in range(1, self.L + 1)]
         self.xent_scratch = torch.empty(max(D.digest_xent_workspace(n), 8), dtype=torch.uint8,
                                         device=dev)
@@ -184,13 +188,15 @@ class DigestWorker:
         gh, ldgh = None, 0
         if self.cfg.halo_grad and l >= 2 and self.part.n_halo > 0:
             gh, ldgh = D.digest_store_grad_buffer(self.store, l - 1)
-        # G_in of layer l is produced already multiplied by 1[H^(l-1) > 0], i.e. it is
-        # D^(l-1); layer l-1 then skips its own masking pass (DIGEST_BWD_G_IS_D).
+        # G_in of layer l is produced already multiplied by 1[H^(l-1) > 0] (the 1-bit
+        # mask of layer l-1), i.e. it is D^(l-1); layer l-1 then skips its own masking
+        # pass (DIGEST_BWD_G_IS_D).
         D.digest_layer_bwd(self.part.handle, xl, xh, ldh, self.W[l - 1], dims[l - 1], dims[l],
                            act, self.layer_order(l), self.saved[l], None, self.G[l],
                            self.GW[l - 1], self.G[l - 1] if l >= 2 else None, self.scratch,
                            stream, flags=D.BWD_G_IS_D if l < self.L else 0,
-                           gin_mask=self.H[l - 1] if l >= 2 else None, G_halo=gh, ld_gh=ldgh)
+                           gin_mask=self.mask_bits[l - 1] if l >= 2 else None, G_halo=gh,
+                           ld_gh=ldgh)
 
     def return_halo_grad(self, l, stream=None):
         """Add the peers' G_halo rows for my nodes into D^(l-1)."""

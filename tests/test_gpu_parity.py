@@ -181,7 +181,41 @@ def test_layer_forward_backward_per_call(d_in, d_out, order):
         torch.cuda.synchronize()
         assert rel(GW2.cpu().numpy(), b["G_W"]) <= TOL
         assert rel(Gin2.cpu().numpy(), b["G_in"] * (gm.numpy() > 0)) <= TOL
+        # the same with the previous layer's ReLU' as a 1-bit mask
+        gmb = torch.from_numpy(pack_bits(gm.numpy() > 0, ld_words(d_in))).cuda()
+        Gin3 = torch.empty_like(Gin)
+        Dm.digest_layer_bwd(p.handle, xl_d, xh_d, d_in, w_d, d_in, d_out, act, order, saved,
+                            None, Dpre, GW2, Gin3, scratch, flags=Dm.BWD_G_IS_D,
+                            gin_mask=(gmb.data_ptr(), gmb.shape[1]))
+        torch.cuda.synchronize()
+        assert torch.equal(Gin3, Gin2)
+        if act:   # the forward's 1-bit mask is exactly 1[H > 0] of its own output
+            bits = saved_bits(Dm, p, d_in, d_out, order, saved)
+            nw = (d_out + 31) // 32   # words past nw are row padding (never read)
+            np.testing.assert_array_equal(bits[:, :nw],
+                                          pack_bits(H.cpu().numpy() > 0, bits.shape[1])[:, :nw])
     p.close()
+
+
+def ld_words(d):
+    return -(-((d + 31) // 32) // 4) * 4
+
+
+def pack_bits(b, ldw):
+    """bool [n, d] -> int32 [n, ldw]: bit j % 32 of word j // 32 = b[:, j]."""
+    n, d = b.shape
+    full = np.zeros((n, ldw * 32), dtype=np.uint64)
+    full[:, :d] = b
+    words = (full.reshape(n, ldw, 32) << np.arange(32, dtype=np.uint64)).sum(axis=2)
+    return words.astype(np.uint32).view(np.int32)
+
+
+def saved_bits(Dm, p, d_in, d_out, order, saved):
+    addr, ldw = Dm.digest_layer_mask(p.handle, d_in, d_out, order, saved)
+    off = addr - saved.data_ptr()
+    assert 0 <= off and off + 4 * p.n_local * ldw <= saved.numel()
+    return saved[off:off + 4 * p.n_local * ldw].view(torch.int32).reshape(
+        p.n_local, ldw).cpu().numpy()
 
 
 def test_layer_empty_halo_and_argument_errors():

@@ -38,14 +38,16 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--rows", type=int, default=2449029)
     ap.add_argument("--iters", type=int, default=5)
+    ap.add_argument("--shapes", default="", help="e.g. 256x48,100x256 (K x N); default all")
     a = ap.parse_args()
+    shapes = [tuple(int(v) for v in s.split("x")) for s in a.shapes.split(",")] if a.shapes else SHAPES
     torch.cuda.set_device(0)
     n = a.rows
     ip = torch.zeros(n + 1, dtype=torch.int64, device="cuda")
     ix = torch.zeros(0, dtype=torch.int32, device="cuda")
     po = torch.zeros(n, dtype=torch.int32, device="cuda")
     p = Partition(ip, ix, po, 1, 0)
-    for K, N in SHAPES:
+    for K, N in shapes:
         A = torch.rand(n, K, device="cuda") - 0.5
         W = torch.rand(K, N, device="cuda") - 0.5
         Z = torch.empty(n, N, device="cuda")
@@ -63,7 +65,35 @@ def main():
                                                saved, None, G, GW, None, scratch), a.iters)
         print(json.dumps({"kernel": "wgrad", "K": K, "N": N, "ms": round(ms, 3),
                           "tflops_alg": round(fl / ms / 1e9, 1)}), flush=True)
-        del A, W, Z, G, saved, scratch
+        # input gradient with the ReLU mask fused in the epilogue: G_in = (G W^T) * [H > 0]
+        # (transform-first order: there the mask is applied in the GEMM epilogue)
+        GI = torch.empty(n, K, device="cuda")
+        Hm = torch.rand(n, K, device="cuda") - 0.5
+        del saved, scratch
+        sv, sc = D.digest_layer_workspace(p.handle, K, N, D.ORDER_XFORM_FIRST)
+        saved = torch.empty(max(sv, 256), dtype=torch.uint8, device="cuda")
+        scratch = torch.empty(max(sc, 256), dtype=torch.uint8, device="cuda")
+        D.digest_layer_fwd(p.handle, A, None, 0, W, K, N, 0, D.ORDER_XFORM_FIRST, Z, saved, scratch)
+        ldw = -(-((K + 31) // 32) // 4) * 4
+        Hb = torch.randint(-2 ** 31, 2 ** 31 - 1, (n, ldw), dtype=torch.int32, device="cuda")
+        for kind, gm in (("float", Hm), ("bits", (Hb.data_ptr(), ldw))):
+            bwd = lambda: D.digest_layer_bwd(p.handle, A, None, 0, W, K, N, 0,  # noqa
+                                             D.ORDER_XFORM_FIRST, saved, None, G, GW, GI,
+                                             scratch, gin_mask=gm)
+            bwd()
+            torch.cuda.synchronize()
+            D.digest_prof_enable(True)
+            for _ in range(a.iters):
+                bwd()
+            torch.cuda.synchronize()
+            det = D.digest_prof_read_detail()
+            D.digest_prof_enable(False)
+            for d in det:
+                if d["cls"] == "gemm" and d["launches"]:
+                    print(json.dumps({"kernel": "bwd_detail", "mask": kind, "K": K, "N": N,
+                                      "tag": d["tag"], "ms": round(d["ms"] / a.iters, 3)}),
+                          flush=True)
+        del A, W, Z, G, saved, scratch, GI, Hm, Hb
 
 
 if __name__ == "__main__":

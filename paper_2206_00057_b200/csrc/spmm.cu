@@ -116,8 +116,12 @@ __device__ __forceinline__ void spmm_row_epilogue(const SpmmArgs& a, int64_t row
 // unrolled, predicated steps of UNR edges per group, so up to STEPS*UNR*VPL 16-byte
 // gathers per lane can be in flight.  Edge-group partial sums are combined with xor
 // shuffles at the end of the row.  All loop counts are warp-uniform.
-template <int LC, int VPL, int UNR>
-__global__ void __launch_bounds__(256) k_spmm(SpmmArgs a) {
+// XR (cross-row pipelining): the warp's NEXT row's bounds are loaded when a row
+// starts and its first (col, val) chunk is loaded during the current row's last
+// gathers, so the row_ptr -> col -> gather dependency chain of a row overlaps the
+// previous row's gathers instead of following them (latency-bound narrow rows).
+template <int LC, int VPL, int UNR, bool XR, int MB>
+__global__ void __launch_bounds__(256, MB) k_spmm(SpmmArgs a) {
   constexpr int EG = 32 / LC;
   constexpr int STEP = EG * UNR;
   constexpr int STEPS = STEP >= 32 ? 1 : 32 / STEP;
@@ -132,23 +136,52 @@ __global__ void __launch_bounds__(256) k_spmm(SpmmArgs a) {
                                         : policy_evict_normal();
   int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t row = warp; row < a.n_rows; row += nwarps) {
-    float4 acc[VPL];
-#pragma unroll
-    for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-    const int64_t beg = a.row_ptr[row];
-    const int64_t end = a.in_len ? beg + a.in_len[row] : a.row_ptr[row + 1];
-    int32_t c_nxt = 0;
-    float v_nxt = 0.f;
+  int64_t beg = 0, end = 0;
+  int32_t c_nxt = 0;
+  float v_nxt = 0.f;
+  if (XR && warp < a.n_rows) {
+    beg = a.row_ptr[warp];
+    end = a.in_len ? beg + a.in_len[warp] : a.row_ptr[warp + 1];
     if (beg + lane < end) {
       c_nxt = ld_stream_i(a.col + beg + lane, pol_s);
       v_nxt = ld_stream_f(a.val + beg + lane, pol_s);
     }
+  }
+  for (int64_t row = warp; row < a.n_rows; row += nwarps) {
+    float4 acc[VPL];
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    int64_t nbeg = 0, nend = 0;
+    if (XR) {
+      const int64_t nrow = row + nwarps;
+      if (nrow < a.n_rows) {
+        nbeg = a.row_ptr[nrow];
+        nend = a.in_len ? nbeg + a.in_len[nrow] : a.row_ptr[nrow + 1];
+      }
+    } else {
+      beg = a.row_ptr[row];
+      end = a.in_len ? beg + a.in_len[row] : a.row_ptr[row + 1];
+      if (beg + lane < end) {
+        c_nxt = ld_stream_i(a.col + beg + lane, pol_s);
+        v_nxt = ld_stream_f(a.val + beg + lane, pol_s);
+      }
+    }
+    // the next row's first chunk (XR): loaded in the last chunk, after its gathers issue
+    auto next_row_chunk = [&]() {
+      c_nxt = 0;
+      v_nxt = 0.f;
+      if (nbeg + lane < nend) {
+        c_nxt = ld_stream_i(a.col + nbeg + lane, pol_s);
+        v_nxt = ld_stream_f(a.val + nbeg + lane, pol_s);
+      }
+    };
+    if (XR && end <= beg) next_row_chunk();
     for (int64_t e0 = beg; e0 < end; e0 += 32) {
       const int32_t c = c_nxt;
       const float v = v_nxt;
       const int cnt = (int)min((int64_t)32, end - e0);
-      if (e0 + 32 + lane < end) {
+      const bool last = e0 + 32 >= end;
+      if (!last && e0 + 32 + lane < end) {
         c_nxt = ld_stream_i(a.col + e0 + 32 + lane, pol_s);
         v_nxt = ld_stream_f(a.val + e0 + 32 + lane, pol_s);
       }
@@ -179,6 +212,7 @@ __global__ void __launch_bounds__(256) k_spmm(SpmmArgs a) {
             t[u][q] = (ok[u] && idx < w4) ? ld_gather(src[u] + 4 * idx, pol[u])
                                           : make_float4(0.f, 0.f, 0.f, 0.f);
           }
+        if (XR && st == 0 && last) next_row_chunk();
 #pragma unroll
         for (int u = 0; u < UNR; ++u)
 #pragma unroll
@@ -207,13 +241,17 @@ __global__ void __launch_bounds__(256) k_spmm(SpmmArgs a) {
         }
       }
     spmm_row_epilogue<LC, VPL>(a, row, lane, cl, g, w4, acc);
+    if (XR) {
+      beg = nbeg;
+      end = nend;
+    }
   }
 }
 
 // Runtime-trip-count variant (no chunk prefetch, default caching): fewer registers,
 // higher occupancy; best for the wide rows (measured).
-template <int LC, int VPL, int UNR>
-__global__ void __launch_bounds__(256) k_spmm_rt(SpmmArgs a) {
+template <int LC, int VPL, int UNR, int MB>
+__global__ void __launch_bounds__(256, MB) k_spmm_rt(SpmmArgs a) {
   constexpr int EG = 32 / LC;
   const int lane = threadIdx.x & 31;
   const int cl = lane % LC;
@@ -299,7 +337,19 @@ __global__ void __launch_bounds__(256) k_spmm_rt(SpmmArgs a) {
 }
 
 
-template <int LC, int VPL, int UNR, bool PF = true>
+template <int LC, int VPL, int UNR, bool PF, int MB>
+digest_status launch_mb(const SpmmArgs& a, cudaStream_t s, int64_t blocks, double bytes,
+                        double flops) {
+  if (PF)
+    DG_LAUNCH_TAG(DIGEST_PROF_SPMM, a.width, s, bytes, flops, (k_spmm<LC, VPL, UNR, false, MB>),
+                  (unsigned)blocks, 256, 0, a);
+  else
+    DG_LAUNCH_TAG(DIGEST_PROF_SPMM, a.width, s, bytes, flops, (k_spmm_rt<LC, VPL, UNR, MB>),
+                  (unsigned)blocks, 256, 0, a);
+  return DIGEST_OK;
+}
+
+template <int LC, int VPL, int UNR, bool PF = true, int MB_DEFAULT = 1>
 digest_status launch(const SpmmArgs& a, cudaStream_t s) {
   int64_t blocks = ceil_div(a.n_rows, 8);
   const int64_t cap = (int64_t)num_sms() * 8 * 8;
@@ -308,12 +358,19 @@ digest_status launch(const SpmmArgs& a, cudaStream_t s) {
   const double w = a.width;
   const double bytes = (double)a.nnz * (8.0 + 4.0 * w) + (double)a.n_rows * (4.0 * w + 8.0);
   const double flops = 2.0 * (double)a.nnz * w;
-  if (PF)
-    DG_LAUNCH_TAG(DIGEST_PROF_SPMM, a.width, s, bytes, flops, (k_spmm<LC, VPL, UNR>),
-                  (unsigned)blocks, 256, 0, a);
-  else
-    DG_LAUNCH_TAG(DIGEST_PROF_SPMM, a.width, s, bytes, flops, (k_spmm_rt<LC, VPL, UNR>),
-                  (unsigned)blocks, 256, 0, a);
+  // MB: minimum resident blocks per SM the register allocation must allow (0 = the
+  // compiler's choice); the narrow widths are latency-bound and gain from occupancy
+  static int mb = -1;
+  if (mb < 0) {
+    const char* e = getenv("DIGEST_SPMM_MB");
+    mb = e ? atoi(e) : 0;
+  }
+  switch (mb ? mb : MB_DEFAULT) {
+    case 4: return launch_mb<LC, VPL, UNR, PF, 4>(a, s, blocks, bytes, flops);
+    case 5: return launch_mb<LC, VPL, UNR, PF, 5>(a, s, blocks, bytes, flops);
+    case 6: return launch_mb<LC, VPL, UNR, PF, 6>(a, s, blocks, bytes, flops);
+    default: return launch_mb<LC, VPL, UNR, PF, 1>(a, s, blocks, bytes, flops);
+  }
   return DIGEST_OK;
 }
 
@@ -388,7 +445,7 @@ digest_status spmm_one(const SpmmArgs& a, cudaStream_t s) {
     }
     if (v == 1) return launch<5, 5, 2, false>(a, s);
     if (v == 2) return launch<5, 5, 2, true>(a, s);
-    return launch<8, 4, 2, false>(a, s);   // measured best for w=100 (9.99 ms)
+    return launch<8, 4, 2, false, 4>(a, s);   // measured best for w=100 (9.2 ms, MB=4)
   }
   if (w4 <= 32) return launch<8, 4, 2, false>(a, s);
   if (w4 <= 64) {
@@ -403,7 +460,7 @@ digest_status spmm_one(const SpmmArgs& a, cudaStream_t s) {
       case 3: return launch<32, 2, 8, false>(a, s);
       case 4: return launch<16, 4, 4, false>(a, s);
       case 5: return launch<32, 2, 2, false>(a, s);
-      default: return launch<32, 2, 4, false>(a, s);
+      default: return launch<32, 2, 4, false, 4>(a, s);   // w=256: 17.98 ms (MB=4) vs 18.95
     }
   }
   if (w4 <= 96) return launch<32, 3, 4, false>(a, s);

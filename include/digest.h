@@ -78,6 +78,27 @@ digest_status digest_comm_init(const uint8_t id_h[128], int32_t nranks, int32_t 
                                digest_comm** out_h);
 digest_status digest_comm_destroy(digest_comm* comm);
 
+/* Peer-memory transport (the alternative to NCCL for C1/C2; the
+ * exchange as loads/stores of the library's own kernels through NVLink/NVSwitch
+ * peer mappings).  Every rank allocates a window (flag words + two gradient slots
+ * of max_grad_count floats) with digest_comm_init_peer, exports its 64-byte CUDA
+ * IPC handle with digest_comm_export, the caller all-gathers the handles over its
+ * process group (rank order) and passes them to digest_comm_connect, which maps
+ * every peer's window.  Works between processes on different GPUs (peer access is
+ * enabled lazily) and between processes sharing one GPU.  A peer communicator may
+ * serve both the store (digest_store_create) and digest_grad_allreduce; its calls
+ * never synchronise the host: producers raise flags with a system-scope release,
+ * consumers spin on them inside their kernels (a wait longer than 30 s traps the
+ * kernel: a CUDA error instead of a hang).  Every rank must issue the same sequence
+ * of collective calls (push/pull/return per level, allreduce). */
+#define DIGEST_IPC_HANDLE_BYTES 64
+digest_status digest_comm_init_peer(int32_t nranks, int32_t rank, int64_t max_grad_count,
+                                    digest_comm** out_h);
+digest_status digest_comm_export(const digest_comm* comm,
+                                 uint8_t handle_h[DIGEST_IPC_HANDLE_BYTES]);
+/* handles_h: nranks x DIGEST_IPC_HANDLE_BYTES, rank order (own entry ignored). */
+digest_status digest_comm_connect(digest_comm* comm, const uint8_t* handles_h);
+
 /* ------------------------------------------------------------------ partition
  * north_star call #1.  Builds, for partition `rank` of `num_parts`, the split of
  * the GCN propagation matrix of Eq. 5 (P_m = P_in + P_out),
@@ -172,6 +193,17 @@ digest_status digest_return_halo_grad(digest_store* store, int32_t level, float*
 /* Current front buffer, its leading dimension and the version it holds. */
 digest_status digest_store_front(const digest_store* store, int32_t level,
                                  const float** front_h, int64_t* ld_h, int64_t* version_h);
+/* Peer transport only: after digest_store_create with a peer communicator, every
+ * rank exports a blob (its halo buffers' IPC handles and its receive offsets; query
+ * the size with blob_h = NULL), the caller all-gathers the blobs in rank order and
+ * passes them to digest_store_connect.  A push then writes straight into the
+ * receivers' back buffers (one fused gather + put + signal kernel, which first waits
+ * for the receiver's pull of the previous exchange); a pull waits for the arrival
+ * flags of the version it exposes; digest_return_halo_grad reads the peers'
+ * gradient slots in place.  digest_store_grad_buffer alternates between two slots on
+ * this transport (each call returns the next one). */
+digest_status digest_store_export(const digest_store* store, uint8_t* blob_h, size_t* bytes_h);
+digest_status digest_store_connect(digest_store* store, const uint8_t* blobs_h, size_t blob_bytes);
 digest_status digest_store_destroy(digest_store* store);
 
 /* ------------------------------------------------------------------ one GCN layer
@@ -257,7 +289,10 @@ digest_status digest_xent(const float* logits, int64_t n, int32_t C, int64_t ld,
 
 /* ------------------------------------------------------------------ AGG and update
  * north_star call #5 (Alg. 1 AGG; update rule P:896): grads <- scale *
- * sum over ranks of grads, in place (ncclAllReduce sum, then a scale kernel).
+ * sum over ranks of grads, in place (ncclAllReduce sum, then a scale kernel; on a
+ * peer communicator: publish into the own window, then every rank sums all ranks'
+ * slots in rank order with the scale fused -- bit-identical to
+ * digest_grad_allreduce_local on the same buffers; count <= max_grad_count).
  * comm == NULL or a 1-rank comm: only the scale is applied. */
 digest_status digest_grad_allreduce(digest_comm* comm, float* grads, int64_t count,
                                     float scale, void* stream);

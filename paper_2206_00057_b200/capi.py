@@ -18,6 +18,7 @@ ACT_NONE, ACT_RELU = 0, 1
 ORDER_AUTO, ORDER_AGG_FIRST, ORDER_XFORM_FIRST = 0, 1, 2
 PUSH_ASYNC, PUSH_L2NORM = 1, 2
 PULL_FLIP, PULL_COPY = 0, 1
+IPC_HANDLE_BYTES = 64
 PROF_SPMM, PROF_GEMM, PROF_PACK, PROF_OTHER = 0, 1, 2, 3
 STATUS = {0: "OK", 1: "E_INVALID", 2: "E_SHAPE", 3: "E_STATE", 4: "E_CUDA", 5: "E_NCCL",
           6: "E_NOMEM", 7: "E_UNSUPPORTED"}
@@ -54,6 +55,11 @@ _SIGS = {
     "digest_comm_unique_id": ([_p], _i32),
     "digest_comm_init": ([_p, _i32, _i32, _p], _i32),
     "digest_comm_destroy": ([_p], _i32),
+    "digest_comm_init_peer": ([_i32, _i32, _i64, _p], _i32),
+    "digest_comm_export": ([_p, _p], _i32),
+    "digest_comm_connect": ([_p, _p], _i32),
+    "digest_store_export": ([_p, _p, _p], _i32),
+    "digest_store_connect": ([_p, _p, _sz], _i32),
     "digest_partition": ([_i64, _i64, _p, _p, _p, _i32, _i32, _u32, _p, _p], _i32),
     "digest_part_get_info": ([_p, _p], _i32),
     "digest_part_export": ([_p] * 11, _i32),
@@ -173,6 +179,25 @@ def digest_comm_destroy(comm):
     _check(lib.digest_comm_destroy(comm))
 
 
+def digest_comm_init_peer(nranks: int, rank: int, max_grad_count: int):
+    out = C.c_void_p()
+    _check(lib.digest_comm_init_peer(nranks, rank, max_grad_count, C.byref(out)))
+    return out.value
+
+
+def digest_comm_export(comm) -> bytes:
+    buf = (C.c_uint8 * IPC_HANDLE_BYTES)()
+    _check(lib.digest_comm_export(comm, buf))
+    return bytes(buf)
+
+
+def digest_comm_connect(comm, handles):
+    """handles: list of every rank's 64-byte export, rank order."""
+    blob = b"".join(handles)
+    buf = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
+    _check(lib.digest_comm_connect(comm, buf))
+
+
 # ------------------------------------------------------------------ partition
 def digest_partition(num_nodes, nnz, indptr, indices, part_of, num_parts, rank, flags=0,
                      stream=None):
@@ -237,6 +262,23 @@ def digest_store_front(store, level):
 
 def digest_store_destroy(store):
     _check(lib.digest_store_destroy(store))
+
+
+def digest_store_export(store) -> bytes:
+    n = C.c_size_t()
+    _check(lib.digest_store_export(store, None, C.byref(n)))
+    buf = (C.c_uint8 * n.value)()
+    _check(lib.digest_store_export(store, buf, C.byref(n)))
+    return bytes(buf)
+
+
+def digest_store_connect(store, blobs):
+    """blobs: every rank's digest_store_export, rank order."""
+    size = len(blobs[0])
+    assert all(len(b) == size for b in blobs)
+    blob = b"".join(blobs)
+    buf = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
+    _check(lib.digest_store_connect(store, buf, size))
 
 
 # ------------------------------------------------------------------ layer

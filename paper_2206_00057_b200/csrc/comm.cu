@@ -17,6 +17,7 @@ namespace dg {
 
 digest_status comm_allreduce_sum(digest_comm* c, float* buf, int64_t count, cudaStream_t s) {
   if (count == 0) return DIGEST_OK;
+  DG_ARG(c->kind == 0, DIGEST_E_INVALID, "not an NCCL communicator");
   DG_NCCL(ncclAllReduce(buf, buf, (size_t)count, ncclFloat, ncclSum, c->comm, s));
   return DIGEST_OK;
 }
@@ -79,6 +80,10 @@ digest_status digest_comm_init(const uint8_t id_h[128], int32_t nranks, int32_t 
 
 digest_status digest_comm_destroy(digest_comm* c) {
   if (!c) return DIGEST_OK;
+  if (c->kind == 1) {
+    cudaDeviceSynchronize();
+    dg::peer_comm_release(c);
+  }
   if (c->comm) ncclCommDestroy(c->comm);
   delete c;
   return DIGEST_OK;

@@ -13,6 +13,7 @@
 //     (async mode, overlapping the next layer: P:250-251).
 // A pull flips front/back (or copies, CUDA-graph safe) only when the back buffer
 // holds a newer version that is older than the current epoch (reading A7).
+#include <cstring>
 #include <vector>
 
 #include "comm_internal.cuh"
@@ -31,7 +32,24 @@ struct Level {
   cudaEvent_t done = nullptr;   // exchange completion (async mode)
   bool inflight = false;
   float* grad_buf = nullptr;    // n_halo x ld: gradient of this part's halo rows (P:816 term)
+                                // (peer transport: two slots, alternating per backward)
   float* ret_recv = nullptr;    // n_send x ld: returned gradients received from peers (NCCL)
+  int64_t last_pull = 0;        // epoch of the last pull call (peer transport)
+  int64_t gseq = 0;             // grad_buffer calls so far (peer transport)
+  size_t halo_bytes = 0;        // bytes of one n_halo x ld buffer
+};
+
+// What a peer needs to reach this store's buffers (digest_store_export / _connect).
+struct PeerBlob {
+  int32_t rank, levels;
+  int64_t halo_rows;             // rows of one halo buffer, max(n_halo, 1) (gradient slot stride)
+  int64_t recv_off[DIGEST_MAX_PARTS];
+  cudaIpcMemHandle_t h[64][3];   // per level: buf[0], buf[1], grad_buf
+};
+struct PeerLevel {
+  float* buf[2];
+  float* grad;
+  size_t slot_bytes;   // the owner's gradient slot stride
 };
 
 // G[idx[j]] += 1[mask[idx[j]] > 0] * src[j]  for the rows of one peer's segment (one launch
@@ -112,6 +130,53 @@ __global__ void k_pack(const float* __restrict__ H, int64_t ldh, const int32_t* 
   }
 }
 
+// Peer transport: the fused gather + put of a push.  Every block first waits until
+// each receiving peer has pulled past the epoch whose flip made its back buffer free
+// (its `pulled` flag), then writes its rows straight into the peers' back buffers
+// through their IPC mappings; the last block to finish fences and raises the
+// receivers' `arrived` flags to the pushed version.
+template <bool NORM>
+__global__ void k_put(const float* __restrict__ H, int64_t ldh, const int32_t* __restrict__ idx,
+                      int64_t n_send, Segs segs, int64_t ld, int w4, dg::FlagWait wait,
+                      dg::FlagSet sig, unsigned* counter) {
+  if (threadIdx.x == 0) dg::wait_flags(wait);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < n_send; r += nw) {
+    int lo = 0, hi = segs.nseg - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (segs.start[mid] <= r) lo = mid; else hi = mid - 1;
+    }
+    const float4* src = reinterpret_cast<const float4*>(H + (int64_t)idx[r] * ldh);
+    float4* dst = reinterpret_cast<float4*>(segs.dst[lo] + (r - segs.start[lo]) * ld);
+    float scale = 1.f;
+    if (NORM) {
+      float ss = 0.f;
+      for (int c = lane; c < w4; c += 32) {
+        float4 v = src[c];
+        ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      scale = ss > 0.f ? 1.f / sqrtf(ss) : 0.f;
+    }
+    for (int c = lane; c < w4; c += 32) {
+      float4 v = src[c];
+      if (NORM) {
+        v.x *= scale;
+        v.y *= scale;
+        v.z *= scale;
+        v.w *= scale;
+      }
+      dst[c] = v;
+    }
+  }
+  if (dg::last_block_done(counter) && threadIdx.x == 0) dg::set_flags(sig);
+}
+
 __global__ void k_copy(const float4* __restrict__ src, float4* __restrict__ dst, int64_t n4) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -127,12 +192,28 @@ struct digest_store {
   std::vector<digest_store*> peers;  // loopback group, index = rank
   cudaStream_t side = nullptr;
   cudaEvent_t packed = nullptr;
+  // peer transport: every rank's buffers mapped here, [rank][level]
+  std::vector<std::vector<PeerLevel>> pl;
+  std::vector<std::vector<int64_t>> peer_recv_off;   // [rank][owner]
+  bool connected = false;
+  unsigned* counters = nullptr;                      // one last-block counter per level
 };
 
 namespace {
 
 void destroy_store(digest_store* st) {
   if (!st) return;
+  if (st->connected) {
+    for (size_t k = 0; k < st->pl.size(); ++k) {
+      if ((int)k == st->part->rank) continue;
+      for (auto& q : st->pl[k]) {
+        if (q.buf[0]) cudaIpcCloseMemHandle(q.buf[0]);
+        if (q.buf[1]) cudaIpcCloseMemHandle(q.buf[1]);
+        if (q.grad) cudaIpcCloseMemHandle(q.grad);
+      }
+    }
+  }
+  cudaFree(st->counters);
   for (auto& L : st->lev) {
     cudaFree(L.buf[0]);
     cudaFree(L.buf[1]);
@@ -210,16 +291,23 @@ digest_status digest_store_create(const digest_part* part, digest_comm* comm, in
       if (cudaMemset(L.buf[b], 0, hb) != cudaSuccess)
         return fail(dg::set_error(DIGEST_E_CUDA, "cudaMemset failed"));
     }
-    if (cudaMalloc(&L.grad_buf, hb) != cudaSuccess ||
-        cudaMemset(L.grad_buf, 0, hb) != cudaSuccess)
+    L.halo_bytes = hb;
+    const size_t gb = dg::is_peer(comm) ? 2 * hb : hb;
+    if (cudaMalloc(&L.grad_buf, gb) != cudaSuccess ||
+        cudaMemset(L.grad_buf, 0, gb) != cudaSuccess)
       return fail(dg::set_error(DIGEST_E_NOMEM, "gradient-return buffer allocation failed"));
-    if (comm && comm->nranks > 1) {
+    if (dg::is_nccl(comm)) {
       if (cudaMalloc(&L.send_buf, sb) != cudaSuccess || cudaMalloc(&L.ret_recv, sb) != cudaSuccess)
         return fail(dg::set_error(DIGEST_E_NOMEM, "send buffer allocation failed"));
     }
     if (cudaEventCreateWithFlags(&L.done, cudaEventDisableTiming) != cudaSuccess)
       return fail(dg::set_error(DIGEST_E_CUDA, "event creation failed"));
   }
+  if (dg::is_peer(comm) &&
+      (cudaMalloc(&st->counters, 64 * sizeof(unsigned)) != cudaSuccess ||
+       cudaMemset(st->counters, 0, 64 * sizeof(unsigned)) != cudaSuccess ||
+       cudaDeviceSynchronize() != cudaSuccess))
+    return fail(dg::set_error(DIGEST_E_NOMEM, "counter allocation failed"));
   if (cudaStreamCreateWithFlags(&st->side, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&st->packed, cudaEventDisableTiming) != cudaSuccess)
     return fail(dg::set_error(DIGEST_E_CUDA, "stream/event creation failed"));
@@ -257,8 +345,42 @@ digest_status digest_push_boundary(digest_store* st, int32_t level, const float*
   const int M = p->num_parts, me = p->rank;
   const int back = 1 - L->front;
   const bool norm = (flags & DIGEST_PUSH_L2NORM) != 0;
-  const bool nccl = st->comm && st->comm->nranks > 1;
-  if (M > 1 && !nccl) {
+  const bool nccl = dg::is_nccl(st->comm);
+  const bool peer = dg::is_peer(st->comm);
+  if (peer) {
+    DG_ARG(st->connected, DIGEST_E_STATE, "peer-transport store is not connected");
+    Segs sg{};
+    sg.nseg = M;
+    dg::FlagWait wt{};
+    dg::FlagSet sig{};
+    wt.value = L->last_pull;
+    sig.value = version;
+    for (int k = 0; k < M; ++k) {
+      sg.start[k] = p->send_off[k];
+      sg.dst[k] = nullptr;
+      if (k == me || p->send_count[k] == 0) continue;
+      // same schedule on every rank => the receiver's back buffer has our index `back`
+      sg.dst[k] = st->pl[k][level - 1].buf[back] + st->peer_recv_off[k][me] * L->ld;
+      wt.ptr[wt.n++] = dg::win_i64(st->comm->peer_win[k], dg::kWinPulled) + (level - 1);
+      sig.ptr[sig.n++] = dg::win_i64(st->comm->peer_win[k], dg::kWinArrived) +
+                         (int64_t)(level - 1) * 64 + me;
+    }
+    sg.start[M] = p->n_send;
+    if (p->n_send > 0) {
+      int64_t blocks = dg::ceil_div(p->n_send, 8);
+      int64_t cap = (int64_t)dg::num_sms() * 16;
+      if (blocks > cap) blocks = cap;
+      double bytes = (double)p->n_send * (8.0 * L->width + 4.0);
+      if (norm)
+        DG_LAUNCH(DIGEST_PROF_PACK, s, bytes, 0, k_put<true>, (unsigned)blocks, 256, 0, H_local, ld,
+                  p->send_idx, p->n_send, sg, L->ld, L->width / 4, wt, sig,
+                  st->counters + (level - 1));
+      else
+        DG_LAUNCH(DIGEST_PROF_PACK, s, bytes, 0, k_put<false>, (unsigned)blocks, 256, 0, H_local,
+                  ld, p->send_idx, p->n_send, sg, L->ld, L->width / 4, wt, sig,
+                  st->counters + (level - 1));
+    }
+  } else if (M > 1 && !nccl) {
     DG_ARG((int)st->peers.size() == M, DIGEST_E_STATE,
            "single-process store of a %d-part graph: link the stores first", M);
     Segs sg{};
@@ -317,7 +439,27 @@ digest_status digest_pull(digest_store* st, int32_t level, int64_t epoch, int32_
     return dg::set_error(DIGEST_E_STATE,
                          "pull at epoch %lld would expose version %lld (pushes are visible to "
                          "later epochs only)", (long long)epoch, (long long)L->ver[back]);
+  const bool peer = dg::is_peer(st->comm);
+  if (peer) DG_ARG(st->connected, DIGEST_E_STATE, "peer-transport store is not connected");
+  dg::FlagSet pulled{};   // peer transport: "my back buffer is free for pushes after `epoch`"
+  if (peer) {
+    pulled.n = 1;
+    pulled.ptr[0] = dg::win_i64(st->comm->win, dg::kWinPulled) + (level - 1);
+    pulled.value = epoch;
+    L->last_pull = epoch;
+  }
   if (L->ver[back] > L->ver[L->front]) {
+    if (peer) {   // wait until every owner's rows of this version have arrived
+      dg::FlagWait arr{};
+      arr.value = L->ver[back];
+      const digest_part* p = st->part;
+      for (int k = 0; k < p->num_parts; ++k)
+        if (k != p->rank && p->recv_count[k] > 0)
+          arr.ptr[arr.n++] = dg::win_i64(st->comm->win, dg::kWinArrived) +
+                             (int64_t)(level - 1) * 64 + k;
+      DG_TRY(dg::flag_sync(arr, mode == DIGEST_PULL_FLIP ? pulled : dg::FlagSet{}, s));
+      if (mode == DIGEST_PULL_FLIP) pulled.n = 0;   // already raised
+    }
     if (L->inflight) {
       DG_CUDA(cudaStreamWaitEvent(s, L->done, 0));
       L->inflight = false;
@@ -336,6 +478,7 @@ digest_status digest_pull(digest_store* st, int32_t level, int64_t epoch, int32_
       L->ver[L->front] = L->ver[back];
     }
   }
+  if (peer && pulled.n) DG_TRY(dg::flag_sync(dg::FlagWait{}, pulled, s));
   if (front_h) *front_h = L->buf[L->front];
   return DIGEST_OK;
 }
@@ -370,7 +513,13 @@ digest_status digest_store_grad_buffer(digest_store* st, int32_t level, float** 
                                        int64_t* ld_h) {
   Level* L;
   DG_TRY(get_level(st, level, &L));
-  if (buf_h) *buf_h = L->grad_buf;
+  float* b = L->grad_buf;
+  if (dg::is_peer(st->comm)) {   // two slots, alternating per backward (see return below)
+    ++L->gseq;
+    b = reinterpret_cast<float*>(reinterpret_cast<char*>(L->grad_buf) +
+                                 (size_t)(L->gseq & 1) * L->halo_bytes);
+  }
+  if (buf_h) *buf_h = b;
   if (ld_h) *ld_h = L->ld;
   return DIGEST_OK;
 }
@@ -389,8 +538,30 @@ digest_status digest_return_halo_grad(digest_store* st, int32_t level, float* G_
   cudaStream_t s = dg::as_stream(stream);
   const int M = p->num_parts, me = p->rank;
   if (M == 1) return DIGEST_OK;
-  const bool nccl = st->comm && st->comm->nranks > 1;
-  if (!nccl)
+  const bool nccl = dg::is_nccl(st->comm);
+  const bool peer = dg::is_peer(st->comm);
+  bool odd = false;
+  if (peer) {
+    // Peer transport, sequence q = this level's grad_buffer calls: raise gready[q] on
+    // every neighbouring part, wait for theirs, then read their slot q%2 in place.  A
+    // slot is rewritten at q+2 only after its owner saw gready[q+1] from every reader,
+    // which each reader raises after finishing its reads of q (stream order).
+    DG_ARG(st->connected, DIGEST_E_STATE, "peer-transport store is not connected");
+    dg::FlagSet sig{};
+    dg::FlagWait wt{};
+    sig.value = wt.value = L->gseq;
+    for (int k = 0; k < M; ++k) {
+      if (k == me || (p->send_count[k] == 0 && p->recv_count[k] == 0)) continue;
+      sig.ptr[sig.n++] = dg::win_i64(st->comm->peer_win[k], dg::kWinGReady) +
+                         (int64_t)(level - 1) * 64 + me;
+      wt.ptr[wt.n++] = dg::win_i64(st->comm->win, dg::kWinGReady) + (int64_t)(level - 1) * 64 + k;
+    }
+    if (sig.n == 0) return DIGEST_OK;   // no neighbouring part: nothing to return
+    DG_ARG(L->gseq > 0, DIGEST_E_STATE, "digest_store_grad_buffer was not called for this level");
+    DG_TRY(dg::flag_sync(dg::FlagWait{}, sig, s));
+    DG_TRY(dg::flag_sync(wt, dg::FlagSet{}, s));
+    odd = (L->gseq & 1) != 0;
+  } else if (!nccl)
     DG_ARG((int)st->peers.size() == M, DIGEST_E_STATE,
            "single-process store of a %d-part graph: link the stores first", M);
   if (nccl) {   // reverse of the push: my halo segment of owner k goes back to k
@@ -410,6 +581,11 @@ digest_status digest_return_halo_grad(digest_store* st, int32_t level, float* G_
     const float* src;
     if (nccl) {
       src = L->ret_recv + p->send_off[k] * L->ld;
+    } else if (peer) {
+      const PeerLevel& q = st->pl[k][level - 1];
+      src = reinterpret_cast<const float*>(reinterpret_cast<const char*>(q.grad) +
+                                           (odd ? q.slot_bytes : 0)) +
+            st->peer_recv_off[k][me] * L->ld;
     } else {
       digest_store* pk = st->peers[k];
       src = pk->lev[level - 1].grad_buf + pk->part->recv_off[me] * L->ld;
@@ -421,6 +597,65 @@ digest_status digest_return_halo_grad(digest_store* st, int32_t level, float* G_
               src, L->ld, p->send_idx + p->send_off[k], n, G_local, ld_g, mask, ld_m,
               L->width / 4);
   }
+  return DIGEST_OK;
+}
+
+digest_status digest_store_export(const digest_store* st, uint8_t* blob_h, size_t* bytes_h) {
+  DG_ARG(st && bytes_h, DIGEST_E_INVALID, "NULL argument");
+  DG_ARG(dg::is_peer(st->comm), DIGEST_E_INVALID, "store does not use the peer transport");
+  *bytes_h = sizeof(PeerBlob);
+  if (!blob_h) return DIGEST_OK;
+  PeerBlob b;
+  std::memset(&b, 0, sizeof(b));
+  b.rank = st->part->rank;
+  b.levels = (int32_t)st->lev.size();
+  for (int k = 0; k < st->part->num_parts; ++k) b.recv_off[k] = st->part->recv_off[k];
+  b.halo_rows = st->part->n_halo > 0 ? st->part->n_halo : 1;
+  for (size_t l = 0; l < st->lev.size(); ++l) {
+    DG_CUDA(cudaIpcGetMemHandle(&b.h[l][0], st->lev[l].buf[0]));
+    DG_CUDA(cudaIpcGetMemHandle(&b.h[l][1], st->lev[l].buf[1]));
+    DG_CUDA(cudaIpcGetMemHandle(&b.h[l][2], st->lev[l].grad_buf));
+  }
+  std::memcpy(blob_h, &b, sizeof(b));
+  return DIGEST_OK;
+}
+
+digest_status digest_store_connect(digest_store* st, const uint8_t* blobs_h, size_t blob_bytes) {
+  DG_ARG(st && blobs_h, DIGEST_E_INVALID, "NULL argument");
+  DG_ARG(dg::is_peer(st->comm), DIGEST_E_INVALID, "store does not use the peer transport");
+  DG_ARG(st->comm->connected, DIGEST_E_STATE, "connect the peer communicator first");
+  DG_ARG(!st->connected, DIGEST_E_STATE, "store already connected");
+  DG_ARG(blob_bytes == sizeof(PeerBlob), DIGEST_E_INVALID, "blob size %zu, expected %zu",
+         blob_bytes, sizeof(PeerBlob));
+  const int M = st->part->num_parts, me = st->part->rank;
+  const size_t nl = st->lev.size();
+  st->pl.assign(M, std::vector<PeerLevel>(nl, PeerLevel{{nullptr, nullptr}, nullptr, 0}));
+  st->peer_recv_off.assign(M, std::vector<int64_t>(DIGEST_MAX_PARTS, 0));
+  for (int k = 0; k < M; ++k) {
+    PeerBlob b;
+    std::memcpy(&b, blobs_h + (size_t)k * sizeof(PeerBlob), sizeof(b));
+    DG_ARG(b.rank == k && b.levels == (int32_t)nl, DIGEST_E_INVALID,
+           "blob %d is from rank %d with %d levels (expected rank %d, %zu levels)", k, b.rank,
+           b.levels, k, nl);
+    for (int j = 0; j < M; ++j) st->peer_recv_off[k][j] = b.recv_off[j];
+    for (size_t l = 0; l < nl; ++l) {
+      if (k == me) {
+        st->pl[k][l] = PeerLevel{{st->lev[l].buf[0], st->lev[l].buf[1]}, st->lev[l].grad_buf,
+                                 st->lev[l].halo_bytes};
+        continue;
+      }
+      void* ptr[3];
+      for (int i = 0; i < 3; ++i) {
+        cudaError_t e = cudaIpcOpenMemHandle(&ptr[i], b.h[l][i], cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess)
+          return dg::set_error(DIGEST_E_CUDA, "cudaIpcOpenMemHandle(rank %d level %zu): %s", k,
+                               l + 1, cudaGetErrorString(e));
+      }
+      const size_t hb = sizeof(float) * (size_t)b.halo_rows * (size_t)st->lev[l].ld;
+      st->pl[k][l] = PeerLevel{{(float*)ptr[0], (float*)ptr[1]}, (float*)ptr[2], hb};
+    }
+  }
+  st->connected = true;
   return DIGEST_OK;
 }
 

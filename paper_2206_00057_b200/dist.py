@@ -6,6 +6,9 @@
 * `check_exchange_plan` -- before the first boundary exchange, verify on every rank that
                        what rank m sends to k equals what k expects from m (otherwise
                        the grouped ncclSend/ncclRecv would hang).
+* `all_gather_bytes`, `connect_peer_comm`, `connect_peer_store` -- bootstrap of the
+                       peer-memory transport: every rank's CUDA IPC handles travel over
+                       the caller's process group, the library maps them.
 """
 from dataclasses import dataclass
 
@@ -65,3 +68,29 @@ def check_exchange_plan(send_count, recv_count, world: int, device="cpu"):
     if torch.diagonal(S).any():
         raise RuntimeError("a rank plans to send boundary rows to itself")
     return S
+
+
+def all_gather_bytes(blob: bytes, world: int):
+    """Every rank's `blob`, rank order (any backend)."""
+    out = [None] * world
+    dist.all_gather_object(out, blob)
+    return out
+
+
+def grad_count(dims):
+    """Floats in the flat weight/gradient buffer of a GCN with widths `dims`."""
+    return sum(int(dims[l]) * int(dims[l + 1]) for l in range(len(dims) - 1))
+
+
+def connect_peer_comm(world: int, rank: int, max_grad_count: int):
+    """Create this rank's peer-memory window and map every peer's (collective)."""
+    from . import capi as D
+    comm = D.digest_comm_init_peer(world, rank, max_grad_count)
+    D.digest_comm_connect(comm, all_gather_bytes(D.digest_comm_export(comm), world))
+    return comm
+
+
+def connect_peer_store(store, world: int):
+    """Map every rank's stale-store buffers into this rank's store (collective)."""
+    from . import capi as D
+    D.digest_store_connect(store, all_gather_bytes(D.digest_store_export(store), world))

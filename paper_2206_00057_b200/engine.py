@@ -9,7 +9,8 @@ Reading A7: all pulls of an epoch happen before any push of that epoch, so pulls
 only ever expose versions < r.  Torch provides memory, streams and process groups.
 
 Two deployments:
-  * DigestWorker with an NCCL communicator: one process per GPU (torchrun);
+  * DigestWorker with an NCCL or peer-memory communicator: one process per GPU
+    (torchrun), or several processes sharing one GPU (peer transport, tests);
   * LoopbackGroup: M partitions in one process on one GPU, stores linked so a push
     writes the peers' back buffers directly (used by the single-GPU tests).
 """
@@ -36,6 +37,7 @@ class TrainConfig:
     fresh: bool = False         # zero-staleness mode (the oracle's mode='fresh')
     cache_l1: bool = False      # aggregate the static layer-1 inputs once
     halo_grad: bool = False     # return P_out^T D W^T to the halo owners
+    transport: str = "nccl"     # multi-process exchange: 'nccl' or 'peer' (CUDA IPC windows)
 
 
 class Partition:
@@ -118,6 +120,9 @@ class DigestWorker:
         self.loss = torch.zeros(1, dtype=torch.float64, device=dev)
         # stale store: levels 1..L-1 (never L)
         self.store = D.digest_store_create(part.handle, comm_halo, list(dims[1:self.L]))
+        if cfg.transport == "peer" and comm_halo is not None and part.num_parts > 1:
+            from .dist import connect_peer_store
+            connect_peer_store(self.store, part.num_parts)   # collective over the process group
         self.pulls = self.pushes = 0
 
     # --------------------------------------------------------------- schedule pieces

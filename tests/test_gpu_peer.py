@@ -1,0 +1,114 @@
+"""Multi-process runs over the peer-memory transport (CUDA IPC windows, flag protocol,
+fused gather+put push, in-kernel waits, rank-order AGG) vs the oracle and vs the
+single-process loopback run of the same partitions.
+
+The pool gives one GPU per call, so the M ranks are M processes sharing cuda:0: the
+same IPC mappings, flags and kernels as one process per GPU, time-sliced instead of
+concurrent.  Bar: per-epoch loss and final weights within 1e-4 of the fp64 oracle
+(north_star), and BIT-identical to the loopback run (same kernels, same summation
+orders), with weights bit-identical across ranks (Alg. 1 AGG invariant)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from synth import make_block_parts, make_inputs, make_random_parts, small_config
+from tests.peer_procs import run_rank
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+
+
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def rel(got, ref):
+    got, ref = np.asarray(got, np.float64), np.asarray(ref, np.float64)
+    return np.abs(got - ref).max() / np.abs(ref).max()
+
+
+GRAPH = dict(num_nodes=1100, nnz=12000, d0=20, hidden=(32, 16), num_classes=6, c_pad=8,
+             train_frac=0.4)
+
+CASES = {
+    "M2_N1_sgd": dict(world=2, parts_seed=None, epochs=5, graph=dict(GRAPH, seed=21),
+                      train=dict(sync_interval=1, lr=0.05, optimizer="sgd")),
+    "M3_N2_adam_random": dict(world=3, parts_seed=4, epochs=6, graph=dict(GRAPH, seed=22),
+                              train=dict(sync_interval=2, lr=0.01, optimizer="adam",
+                                         async_push=True)),
+    "M4_N3_copy": dict(world=4, parts_seed=None, epochs=7, graph=dict(GRAPH, seed=23),
+                       train=dict(sync_interval=3, lr=0.05, optimizer="sgd", pull_mode=1)),
+    "M2_fresh": dict(world=2, parts_seed=None, epochs=3, graph=dict(GRAPH, seed=24),
+                     train=dict(sync_interval=1, lr=0.05, optimizer="sgd", fresh=True)),
+    "M3_fresh_halo_grad": dict(world=3, parts_seed=9, epochs=3, graph=dict(GRAPH, seed=25),
+                               train=dict(sync_interval=1, lr=0.05, optimizer="sgd", fresh=True,
+                                          halo_grad=True)),
+    "M3_stale_halo_grad": dict(world=3, parts_seed=9, epochs=4, graph=dict(GRAPH, seed=26),
+                               train=dict(sync_interval=2, lr=0.05, optimizer="sgd",
+                                          halo_grad=True)),
+}
+
+
+def loopback(spec, cfg, inp, part):
+    from paper_2206_00057_b200.engine import TrainConfig, build_workers, LoopbackGroup
+    M = spec["world"]
+    tc = TrainConfig(dims=cfg.dims, num_classes=cfg.num_classes, **spec["train"])
+    ws = build_workers(inp.indptr, inp.indices, inp.x, inp.y, inp.train_mask, inp.weights, part,
+                       M, tc)
+    grp = LoopbackGroup(ws)
+    losses = []
+    for r in range(1, spec["epochs"] + 1):
+        grp.epoch(r)
+        torch.cuda.synchronize()
+        losses.append([float(w.loss.item()) for w in ws])
+    W = ws[0].W_flat.cpu().numpy()
+    grp.close()
+    return np.array(losses).T, W
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("name", list(CASES))
+def test_peer_transport_multiprocess(name, tmp_path):
+    import torch.multiprocessing as mp
+    spec = CASES[name]
+    M = spec["world"]
+    out = str(tmp_path / "res.npz")
+    mp.start_processes(run_rank, args=(M, free_port(), spec, out), nprocs=M, join=True,
+                       start_method="spawn")
+    res = np.load(out)
+    cfg = small_config(**spec["graph"])
+    inp = make_inputs(cfg)
+    part = (make_block_parts(cfg, M) if spec["parts_seed"] is None
+            else make_random_parts(cfg.num_nodes, M, spec["parts_seed"]))
+    tr = spec["train"]
+    run = oracle.oracle_train(inp.indptr, inp.indices, inp.x, inp.y, inp.train_mask, inp.weights,
+                              cfg.num_classes, part, M, sync_interval=tr["sync_interval"],
+                              epochs=spec["epochs"], lr=tr["lr"], optimizer=tr["optimizer"],
+                              mode="fresh" if tr.get("fresh") else "stale",
+                              halo_grad="same_epoch" if tr.get("halo_grad") else "none")
+    loss = res["loss"].sum(axis=0)
+    for r, rec in enumerate(run.records):
+        assert abs(loss[r] - rec.loss) <= TOL * abs(rec.loss), (r, loss[r], rec.loss)
+    W = res["W"]
+    for k in range(1, M):                       # AGG: bit-identical weights on every rank
+        assert W[k].tobytes() == W[0].tobytes(), k
+    wref = np.concatenate([w.ravel() for w in run.weights])
+    assert rel(W[0], wref) <= TOL
+    assert (res["launches"] > 0).all()
+    # the multi-process run is the loopback run, bit for bit
+    lb_loss, lb_W = loopback(spec, cfg, inp, part)
+    assert res["loss"].tobytes() == lb_loss.tobytes()
+    assert W[0].tobytes() == lb_W.tobytes()

@@ -44,6 +44,12 @@ def parse():
                     help="override the config's N_sync (the Fig. 6 sweep, SURVEY f1)")
     ap.add_argument("--fresh", action="store_true",
                     help="zero-staleness exchange every level and epoch (SURVEY f1)")
+    ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
+                    help="N>1 exchange: library kernels over CUDA-IPC peer windows (default) "
+                         "or NCCL send/recv + allreduce")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="testing only: every rank on cuda:0, gloo process group (timings are "
+                         "time-sliced, not a scaling number)")
     ap.add_argument("--cache-l1", action="store_true",
                     help="aggregate the static layer-1 inputs once (SURVEY f3 (i)); off by default")
     return ap.parse_args()
@@ -164,9 +170,15 @@ def run_reference(a, rank, world):
 def run_ours(a, rank, world, local):
     import torch
     import torch.distributed as dist
+    if a.share_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if a.share_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    coll_dev = "cpu" if a.share_gpu else "cuda"
     from paper_2206_00057_b200 import capi as D
     from paper_2206_00057_b200.engine import TrainConfig, build_workers
     from synth import get_config, make_inputs, make_block_parts
@@ -179,16 +191,19 @@ def run_ours(a, rank, world, local):
     t_gen = time.time() - t0
 
     comm_grad = comm_halo = None
-    if world > 1:
+    if world > 1 and a.transport == "nccl":
         from paper_2206_00057_b200.dist import broadcast_ids
-        ids = broadcast_ids(D.digest_comm_unique_id, 2, rank, device="cuda")
+        ids = broadcast_ids(D.digest_comm_unique_id, 2, rank, device=coll_dev)
         comm_grad = D.digest_comm_init(ids[0], world, rank)
         comm_halo = D.digest_comm_init(ids[1], world, rank)
+    elif world > 1:
+        from paper_2206_00057_b200.dist import connect_peer_comm, grad_count
+        comm_grad = comm_halo = connect_peer_comm(world, rank, grad_count(cfg.dims))
 
     n_sync = a.sync_interval or cfg.sync_interval
     tc = TrainConfig(dims=cfg.dims, num_classes=cfg.num_classes, sync_interval=n_sync,
                      lr=0.01, optimizer="adam", async_push=(a.mode == "async"),
-                     cache_l1=a.cache_l1, fresh=a.fresh)
+                     cache_l1=a.cache_l1, fresh=a.fresh, transport=a.transport)
     t1 = time.time()
     (w,) = build_workers(inp.indptr, inp.indices, inp.x, inp.y, inp.train_mask, inp.weights,
                          part_of, M, tc, ranks=[rank], comm_grad=comm_grad, comm_halo=comm_halo)
@@ -197,7 +212,7 @@ def run_ours(a, rank, world, local):
     info = w.part.info
     if world > 1:   # refuse to start if the per-peer boundary counts disagree (NCCL would hang)
         from paper_2206_00057_b200.dist import check_exchange_plan
-        check_exchange_plan(info.send_count, info.recv_count, world, device="cuda")
+        check_exchange_plan(info.send_count, info.recv_count, world, device=coll_dev)
     stream = torch.cuda.current_stream()
 
     def barrier():
@@ -208,7 +223,7 @@ def run_ours(a, rank, world, local):
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -295,7 +310,7 @@ def run_ours(a, rank, world, local):
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": a.config, "num_nodes": cfg.num_nodes, "nnz": cfg.nnz,
                        "parts": M, "dims": list(cfg.dims), "sync_interval": n_sync,
-                       "fresh": a.fresh,
+                       "fresh": a.fresh, "transport": a.transport if world > 1 else None,
                        "mode": a.mode, "cache_l1": a.cache_l1,
                        "n_local": info.n_local, "n_halo": info.n_halo,
                        "nnz_local": info.nnz, "l2": "inputs larger than L2 (no flush needed)"},
@@ -313,10 +328,13 @@ def run_ours(a, rank, world, local):
             "setup_s": {"generate": t_gen, "partition_and_setup": t_part},
         }
         print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()      # no rank unmaps a buffer a peer may still read
     w.close()
     if world > 1:
         D.digest_comm_destroy(comm_grad)
-        D.digest_comm_destroy(comm_halo)
+        if comm_halo != comm_grad:
+            D.digest_comm_destroy(comm_halo)
         dist.destroy_process_group()
 
 

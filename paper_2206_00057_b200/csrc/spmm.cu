@@ -337,15 +337,51 @@ __global__ void __launch_bounds__(256, MB) k_spmm_rt(SpmmArgs a) {
 }
 
 
+// Grid: at most the number of CTAs that are resident at once (a persistent grid).  The
+// rows are dealt round-robin (row = warp + k * nwarps), so with every warp resident the
+// rows in flight form one narrow, monotonically advancing window -- a graph block's
+// gathered source rows stay in L2 while the window sweeps it (with column slabs, see
+// spmm_slab_width).  An oversubscribed grid would let each CTA sweep the whole row range
+// over its lifetime and scatter the window across the graph.
+template <typename K>
+int64_t resident_ctas(K kern) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  return (int64_t)per_sm * num_sms();
+}
+
+// DIGEST_SPMM_GRID: 0 persistent, 1 oversubscribed (64 CTAs/SM cap), unset = by mean row
+// length: persistent below 128 nonzeros per row (measured, products M=1 w=256/100/48:
+// 17.9/9.3/5.2 -> 16.6/8.4/4.6 ms), oversubscribed for long rows (Reddit, ~490 per row:
+// w=256 12.4 vs 13.6 ms persistent).
+bool spmm_persistent(const SpmmArgs& a) {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("DIGEST_SPMM_GRID");
+    v = e ? atoi(e) : -1;
+  }
+  if (v >= 0) return v == 0;
+  return a.nnz < 128 * a.n_rows;
+}
+
 template <int LC, int VPL, int UNR, bool PF, int MB>
 digest_status launch_mb(const SpmmArgs& a, cudaStream_t s, int64_t blocks, double bytes,
                         double flops) {
-  if (PF)
-    DG_LAUNCH_TAG(DIGEST_PROF_SPMM, a.width, s, bytes, flops, (k_spmm<LC, VPL, UNR, false, MB>),
+  if (PF) {
+    static const int64_t cap = resident_ctas(k_spmm<LC, VPL, UNR, false, MB>);
+    if (spmm_persistent(a) && blocks > cap) blocks = cap;
+    DG_LAUNCH_TAG(DIGEST_PROF_SPMM, a.full_width > 0 ? a.full_width : a.width, s, bytes, flops,
+                  (k_spmm<LC, VPL, UNR, false, MB>),
                   (unsigned)blocks, 256, 0, a);
-  else
-    DG_LAUNCH_TAG(DIGEST_PROF_SPMM, a.width, s, bytes, flops, (k_spmm_rt<LC, VPL, UNR, MB>),
+  } else {
+    static const int64_t cap = resident_ctas(k_spmm_rt<LC, VPL, UNR, MB>);
+    if (spmm_persistent(a) && blocks > cap) blocks = cap;
+    DG_LAUNCH_TAG(DIGEST_PROF_SPMM, a.full_width > 0 ? a.full_width : a.width, s, bytes, flops,
+                  (k_spmm_rt<LC, VPL, UNR, MB>),
                   (unsigned)blocks, 256, 0, a);
+  }
   return DIGEST_OK;
 }
 
@@ -355,9 +391,12 @@ digest_status launch(const SpmmArgs& a, cudaStream_t s) {
   const int64_t cap = (int64_t)num_sms() * 8 * 8;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  const double w = a.width;
-  const double bytes = (double)a.nnz * (8.0 + 4.0 * w) + (double)a.n_rows * (4.0 * w + 8.0);
-  const double flops = 2.0 * (double)a.nnz * w;
+  // algorithmic bytes/flops of the whole product (SURVEY §8.d.4 edge-gather model); a
+  // column-slab launch declares its share slab/W of them, tagged with the full width W
+  const double W = a.full_width > 0 ? a.full_width : a.width;
+  const double frac = a.width / W;
+  const double bytes = frac * ((double)a.nnz * (8.0 + 4.0 * W) + (double)a.n_rows * (4.0 * W + 8.0));
+  const double flops = 2.0 * (double)a.nnz * a.width;
   // MB: minimum resident blocks per SM the register allocation must allow (0 = the
   // compiler's choice); the narrow widths are latency-bound and gain from occupancy
   static int mb = -1;
@@ -404,14 +443,18 @@ digest_status spmm(const SpmmArgs& a0, cudaStream_t s) {
   DG_ARG(a.width > 0 && a.width % 4 == 0, DIGEST_E_INVALID,
          "SpMM width %d must be a positive multiple of 4", a.width);
   const int slab = spmm_slab_width(a);
-  if (slab <= 0 || slab % 4 != 0 || slab >= a.width || a.mbits || a.obits) return spmm_one(a, s);
+  if (slab <= 0 || slab % 4 != 0 || slab >= a.width || ((a.mbits || a.obits) && slab % 32 != 0))
+    return spmm_one(a, s);
   for (int c0 = 0; c0 < a.width; c0 += slab) {
     SpmmArgs b = a;
     b.X0 = a.X0 + c0;
     b.X1 = a.X1 + c0;
     b.Y = a.Y + c0;
     if (a.mask) b.mask = a.mask + c0;
+    if (a.mbits) b.mbits = a.mbits + c0 / 32;   // 1-bit masks: one word per 32 columns
+    if (a.obits) b.obits = a.obits + c0 / 32;
     b.width = a.width - c0 < slab ? a.width - c0 : slab;
+    b.full_width = a.width;
     DG_TRY(spmm_one(b, s));
   }
   return DIGEST_OK;

@@ -300,6 +300,27 @@ digest_status digest_grad_allreduce(digest_comm* comm, float* grads, int64_t cou
  * scale * (bufs[0] + ... + bufs[n-1]) summed in index order. */
 digest_status digest_grad_allreduce_local(float* const* bufs_h, int32_t n, int64_t count,
                                           float scale, void* stream);
+/* DIGEST-A parameter server ("downloads/uploads parameters from the PS without
+ * blindly waiting for the slowest subgraph"; P:243 aggregation moved into the subgraph
+ * loop).  Upload = mixing W_global <- (1 - alpha) W_global + alpha W_local (reading R1,
+ * S:383/S:426; alpha in (0, 1], 1/M by default), download = W_local <- W_global.
+ * digest_ps_mix / digest_ps_download: W_global is a caller device buffer (one process;
+ * the caller orders the uploads).  digest_ps_*_peer: W_global lives in rank 0's
+ * peer-memory window (count <= the window's max_grad_count); each call is one kernel
+ * that holds a system-scope lock in that window, so uploads from independent processes
+ * are atomic and no rank ever waits for another's epoch.  digest_ps_init_peer (rank 0
+ * only) sets W_global; digest_ps_updates_peer reads the upload count (synchronous). */
+digest_status digest_ps_mix(float* W_global, const float* W_local, int64_t count, float alpha,
+                            void* stream);
+digest_status digest_ps_download(const float* W_global, float* W_local, int64_t count,
+                                 void* stream);
+digest_status digest_ps_init_peer(digest_comm* comm, const float* W0, int64_t count,
+                                  void* stream);
+digest_status digest_ps_upload_peer(digest_comm* comm, const float* W_local, int64_t count,
+                                    float alpha, void* stream);
+digest_status digest_ps_download_peer(digest_comm* comm, float* W_local, int64_t count,
+                                      void* stream);
+digest_status digest_ps_updates_peer(digest_comm* comm, int64_t* updates_h);
 /* Alg. 1 local update W <- W - lr*G. */
 digest_status digest_sgd_step(float* W, const float* G, int64_t count, float lr, void* stream);
 /* Adam, bias-corrected, step >= 1. */

@@ -85,6 +85,12 @@ _SIGS = {
     "digest_grad_allreduce": ([_p, _p, _i64, _f32, _p], _i32),
     "digest_grad_allreduce_local": ([_p, _i32, _i64, _f32, _p], _i32),
     "digest_sgd_step": ([_p, _p, _i64, _f32, _p], _i32),
+    "digest_ps_mix": ([_p, _p, _i64, _f32, _p], _i32),
+    "digest_ps_download": ([_p, _p, _i64, _p], _i32),
+    "digest_ps_init_peer": ([_p, _p, _i64, _p], _i32),
+    "digest_ps_upload_peer": ([_p, _p, _i64, _f32, _p], _i32),
+    "digest_ps_download_peer": ([_p, _p, _i64, _p], _i32),
+    "digest_ps_updates_peer": ([_p, _p], _i32),
     "digest_adam_step": ([_p, _p, _p, _p, _i64, _f32, _f32, _f32, _f32, _i64, _p], _i32),
     "digest_gemm": ([_p, _i64, _p, _i64, _p, _i64, _i64, _i32, _i32, _u32, _p], _i32),
 }
@@ -385,3 +391,32 @@ def digest_gemm(A, B, Cm, relu=False, stream=None):
     N = B.shape[1]
     _check(lib.digest_gemm(ptr(A), ld_of(A), ptr(B), ld_of(B), ptr(Cm), ld_of(Cm), M, N, K,
                            1 if relu else 0, stream_ptr(stream)))
+
+
+# ------------------------------------------------------------------ DIGEST-A parameter server
+def digest_ps_mix(W_global, W_local, alpha, stream=None):
+    _check(lib.digest_ps_mix(ptr(W_global), ptr(W_local), W_local.numel(), alpha,
+                             stream_ptr(stream)))
+
+
+def digest_ps_download(W_global, W_local, stream=None):
+    _check(lib.digest_ps_download(ptr(W_global), ptr(W_local), W_local.numel(), stream_ptr(stream)))
+
+
+def digest_ps_init_peer(comm, W0, stream=None):
+    _check(lib.digest_ps_init_peer(comm, ptr(W0), W0.numel(), stream_ptr(stream)))
+
+
+def digest_ps_upload_peer(comm, W_local, alpha, stream=None):
+    _check(lib.digest_ps_upload_peer(comm, ptr(W_local), W_local.numel(), alpha,
+                                     stream_ptr(stream)))
+
+
+def digest_ps_download_peer(comm, W_local, stream=None):
+    _check(lib.digest_ps_download_peer(comm, ptr(W_local), W_local.numel(), stream_ptr(stream)))
+
+
+def digest_ps_updates_peer(comm) -> int:
+    n = C.c_int64()
+    _check(lib.digest_ps_updates_peer(comm, C.byref(n)))
+    return n.value

@@ -14,7 +14,8 @@ constexpr size_t kWinArrived = 0;                                   // int64 [le
 constexpr size_t kWinPulled = kWinArrived + 8 * kWinLevels * 64;    // int64 [level]: last pull epoch of the owner
 constexpr size_t kWinGReady = kWinPulled + 8 * kWinLevels;          // int64 [level][src]: halo-grad slot ready (seq)
 constexpr size_t kWinArReady = kWinGReady + 8 * kWinLevels * 64;    // int64 [src]: allreduce slot ready (seq)
-constexpr size_t kWinSlots = (kWinArReady + 8 * 64 + 4095) / 4096 * 4096;  // float [2][max_grad]
+constexpr size_t kWinPs = kWinArReady + 8 * 64;                      // int64 [2]: PS lock, PS updates
+constexpr size_t kWinSlots = (kWinPs + 16 + 4095) / 4096 * 4096;    // float [3][max_grad]: 2 AGG slots, PS W
 }  // namespace dg
 
 struct digest_comm {

@@ -112,7 +112,7 @@ digest_status digest_comm_init_peer(int32_t nranks, int32_t rank, int64_t max_gr
   c->nranks = nranks;
   c->rank = rank;
   c->max_grad = dg::round_up(max_grad_count, 4);
-  const size_t bytes = dg::kWinSlots + sizeof(float) * 2 * (size_t)(c->max_grad > 0 ? c->max_grad : 4);
+  const size_t bytes = dg::kWinSlots + sizeof(float) * 3 * (size_t)(c->max_grad > 0 ? c->max_grad : 4);
   if (cudaMalloc(&c->win, bytes) != cudaSuccess || cudaMemset(c->win, 0, bytes) != cudaSuccess ||
       cudaMalloc(&c->counters, 256 * sizeof(unsigned)) != cudaSuccess ||
       cudaMemset(c->counters, 0, 256 * sizeof(unsigned)) != cudaSuccess ||

@@ -238,10 +238,58 @@ class DigestWorker:
         self.allreduce(stream)
         self.update(stream)
 
+    def local_epoch(self, r, stream=None):
+        """One DIGEST-A local epoch r (no AGG inside; the PS mixes afterwards):
+        Alg. 1's pull/push guards on this worker's own counter, forward, loss, backward
+        and the local optimizer step."""
+        sched = Schedule(self.cfg.sync_interval)
+        if sched.pull(r):
+            self.pull(r, stream)
+        self.forward(r, sched.push(r), stream)
+        self.loss_and_backward(stream)
+        self.update(stream)
+
     def close(self):
         if self.store:
             D.digest_store_destroy(self.store)
             self.store = None
+
+
+class AsyncLoopbackGroup:
+    """DIGEST-A for M partitions in one process.
+
+    Asynchrony is an input: `event(m)` runs worker m's next local epoch -- download
+    W_global, local epoch (pull/push keyed on its own counter), upload (PS mixing,
+    digest_ps_mix) -- so a seeded event list (synth.async_sched: discrete-event clock
+    with stragglers) fixes the interleaving and the run is comparable with the oracle.
+    The stale store runs in COPY mode: a part's back buffer always holds every owner's
+    latest pushed rows and a pull copies them (a flip could re-expose an owner's older
+    rows when owners push at different rates)."""
+
+    def __init__(self, workers, alpha=None):
+        self.workers = workers
+        M = len(workers)
+        self.alpha = 1.0 / M if alpha is None else float(alpha)
+        for w in workers:
+            if w.cfg.pull_mode != D.PULL_COPY:
+                raise ValueError("DIGEST-A needs pull_mode=PULL_COPY")
+        if M > 1:
+            D.digest_store_link([w.store for w in workers])
+        self.W_global = workers[0].W_flat.clone()
+        self.r = [0] * M
+        self.ps_updates = 0
+
+    def event(self, m, stream=None):
+        w = self.workers[m]
+        self.r[m] += 1
+        D.digest_ps_download(self.W_global, w.W_flat, stream)
+        w.local_epoch(self.r[m], stream)
+        D.digest_ps_mix(self.W_global, w.W_flat, self.alpha, stream)
+        self.ps_updates += 1
+
+    def close(self):
+        for w in self.workers:
+            w.close()
 
 
 class LoopbackGroup:
@@ -295,8 +343,12 @@ class LoopbackGroup:
 
 
 def build_workers(indptr, indices, x, y, train_mask, weights, part_of, num_parts, cfg: TrainConfig,
-                  ranks=None, comm_grad=None, comm_halo=None, device="cuda"):
+                  ranks=None, comm_grad=None, comm_halo=None, device="cuda",
+                  loss_weighting="count"):
     """Partition on the device and set up workers for `ranks` (default: all parts).
+
+    loss_weighting: 'count' = 1/#train over the whole graph (A12, the synchronous AGG of
+    gradient sums); 'local' = 1/#train of the part (DIGEST-A's local objective, Eq. 3).
 
     indptr/indices/part_of/x/y/train_mask: host numpy arrays (the synthetic inputs).
     The layer-1 inputs X[V_m] and X[H_m] are gathered on the device by digest_gather_rows."""
@@ -307,7 +359,8 @@ def build_workers(indptr, indices, x, y, train_mask, weights, part_of, num_parts
     d_x = torch.as_tensor(x, dtype=torch.float32).to(device)
     d_y = torch.as_tensor(y, dtype=torch.int32).to(device)
     d_t = torch.as_tensor(train_mask, dtype=torch.uint8).to(device)
-    w_loss = 1.0 / max(1, int(np.asarray(train_mask).astype(bool).sum()))   # count weighting (A12)
+    tmask = np.asarray(train_mask).astype(bool)
+    w_loss = 1.0 / max(1, int(tmask.sum()))   # count weighting (A12)
     workers = []
     for r in ranks:
         p = Partition(d_ip, d_ix, d_po, num_parts, r)
@@ -321,6 +374,9 @@ def build_workers(indptr, indices, x, y, train_mask, weights, part_of, num_parts
             D.digest_gather_rows(d_x, hids, xh)
         lab = d_y[ids.long()].contiguous()
         msk = d_t[ids.long()].contiguous()
-        workers.append(DigestWorker(p, cfg, xl, xh, lab, msk, weights, w_loss,
+        wl = w_loss
+        if loss_weighting == "local":
+            wl = 1.0 / max(1, int(tmask[np.asarray(part_of) == r].sum()))
+        workers.append(DigestWorker(p, cfg, xl, xh, lab, msk, weights, wl,
                                     comm_grad, comm_halo))
     return workers

@@ -150,8 +150,17 @@ digest_status digest_part_destroy(digest_part* part);
  * partitions of a loopback run) are linked with digest_store_link so a push
  * writes straight into the peers' back buffers (a fused gather + put). */
 typedef struct digest_store digest_store;
-enum { DIGEST_PUSH_ASYNC = 1u, DIGEST_PUSH_L2NORM = 2u };
-enum { DIGEST_PULL_FLIP = 0, DIGEST_PULL_COPY = 1 };
+enum { DIGEST_PUSH_ASYNC = 1u, DIGEST_PUSH_L2NORM = 2u, DIGEST_PUSH_NOWAIT = 4u };
+enum { DIGEST_PULL_FLIP = 0, DIGEST_PULL_COPY = 1, DIGEST_PULL_SNAPSHOT = 2 };
+/* DIGEST-A on the peer transport ("pulls/pushes stale representations of other
+ * subgraphs from the shared KVS ... without blindly waiting"): a push with
+ * DIGEST_PUSH_NOWAIT does not wait for the receiver; it brackets its rows with a
+ * per-(level, owner) sequence word (odd while writing, even when complete), and a pull
+ * in DIGEST_PULL_SNAPSHOT mode copies every owner's segment back -> front, retrying a
+ * segment whose sequence word changed or was odd during the copy -- each owner's rows
+ * are taken from one push (key atomicity, SPEC "Concurrency Model").  Every rank of a
+ * store must use the same mode.  On a single-process (linked) store both behave like
+ * the plain push and DIGEST_PULL_COPY. */
 
 digest_status digest_store_create(const digest_part* part, digest_comm* comm,
                                   int32_t num_levels, const int32_t* width_h,
@@ -321,6 +330,9 @@ digest_status digest_ps_upload_peer(digest_comm* comm, const float* W_local, int
 digest_status digest_ps_download_peer(digest_comm* comm, float* W_local, int64_t count,
                                       void* stream);
 digest_status digest_ps_updates_peer(digest_comm* comm, int64_t* updates_h);
+/* Straggler injection ("a random delay ... added to the chosen straggler"; SPEC
+ * inject_delay): a one-thread kernel that spins for `ns` nanoseconds on `stream`. */
+digest_status digest_delay(int64_t ns, void* stream);
 /* Alg. 1 local update W <- W - lr*G. */
 digest_status digest_sgd_step(float* W, const float* G, int64_t count, float lr, void* stream);
 /* Adam, bias-corrected, step >= 1. */

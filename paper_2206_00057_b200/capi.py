@@ -16,8 +16,8 @@ LIB_PATH = os.path.join(_HERE, "libdigest.so")
 DIGEST_MAX_PARTS = 64
 ACT_NONE, ACT_RELU = 0, 1
 ORDER_AUTO, ORDER_AGG_FIRST, ORDER_XFORM_FIRST = 0, 1, 2
-PUSH_ASYNC, PUSH_L2NORM = 1, 2
-PULL_FLIP, PULL_COPY = 0, 1
+PUSH_ASYNC, PUSH_L2NORM, PUSH_NOWAIT = 1, 2, 4
+PULL_FLIP, PULL_COPY, PULL_SNAPSHOT = 0, 1, 2
 IPC_HANDLE_BYTES = 64
 PROF_SPMM, PROF_GEMM, PROF_PACK, PROF_OTHER = 0, 1, 2, 3
 STATUS = {0: "OK", 1: "E_INVALID", 2: "E_SHAPE", 3: "E_STATE", 4: "E_CUDA", 5: "E_NCCL",
@@ -91,6 +91,7 @@ _SIGS = {
     "digest_ps_upload_peer": ([_p, _p, _i64, _f32, _p], _i32),
     "digest_ps_download_peer": ([_p, _p, _i64, _p], _i32),
     "digest_ps_updates_peer": ([_p, _p], _i32),
+    "digest_delay": ([_i64, _p], _i32),
     "digest_adam_step": ([_p, _p, _p, _p, _i64, _f32, _f32, _f32, _f32, _i64, _p], _i32),
     "digest_gemm": ([_p, _i64, _p, _i64, _p, _i64, _i64, _i32, _i32, _u32, _p], _i32),
 }
@@ -420,3 +421,7 @@ def digest_ps_updates_peer(comm) -> int:
     n = C.c_int64()
     _check(lib.digest_ps_updates_peer(comm, C.byref(n)))
     return n.value
+
+
+def digest_delay(ns: int, stream=None):
+    _check(lib.digest_delay(int(ns), stream_ptr(stream)))

@@ -67,6 +67,15 @@ __global__ void __launch_bounds__(1024) k_ps_locked(float* Wg, float* Wm, int64_
   }
 }
 
+__global__ void k_delay(int64_t ns) {
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    __nanosleep(1000);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while ((int64_t)(t - t0) < ns);
+}
+
 unsigned blocks_for(int64_t n) {
   int64_t b = dg::ceil_div(n, 256);
   int64_t cap = (int64_t)dg::num_sms() * 4;
@@ -133,6 +142,13 @@ digest_status digest_ps_updates_peer(digest_comm* comm, int64_t* updates_h) {
          "bad argument");
   DG_CUDA(cudaMemcpy(updates_h, dg::win_i64(comm->peer_win[0], dg::kWinPs) + 1, sizeof(int64_t),
                      cudaMemcpyDeviceToHost));
+  return DIGEST_OK;
+}
+
+digest_status digest_delay(int64_t ns, void* stream) {
+  DG_ARG(ns >= 0, DIGEST_E_INVALID, "negative delay");
+  if (ns == 0) return DIGEST_OK;
+  DG_LAUNCH(DIGEST_PROF_OTHER, dg::as_stream(stream), 0, 0, k_delay, 1, 1, 0, ns);
   return DIGEST_OK;
 }
 

@@ -124,7 +124,7 @@ template <int LC, int VPL, int UNR, bool XR, int MB>
 __global__ void __launch_bounds__(256, MB) k_spmm(SpmmArgs a) {
   constexpr int EG = 32 / LC;
   constexpr int STEP = EG * UNR;
-  constexpr int STEPS = STEP >= 32 ? 1 : 32 / STEP;
+  constexpr int STEPS = (32 + STEP - 1) / STEP;   // cover all 32 pairs of a chunk
   const int lane = threadIdx.x & 31;
   const int cl = lane % LC;
   const int g = lane / LC;
@@ -473,11 +473,13 @@ digest_status spmm_one(const SpmmArgs& a, cudaStream_t s) {
       const char* e = getenv("DIGEST_SPMM_V12");
       v = e ? atoi(e) : 0;
     }
-    if (v == 1) return launch<4, 3, 2>(a, s);
+    if (v == 1) return launch<4, 3, 4>(a, s);
     if (v == 2) return launch<4, 3, 2, false>(a, s);
     if (v == 3) return launch<4, 3, 4, false>(a, s);
     if (v == 4) return launch<8, 2, 2>(a, s);
-    return launch<4, 3, 4>(a, s);   // measured best for w=48 (4.60 ms vs 5.56 ms, products M=1)
+    // measured best for w=48 with the persistent grid (products M=1): 4.11 ms vs 4.30 ms
+    // for <4,3,4> (profiles/r1_spmm_variant_sweep.log)
+    return launch<4, 3, 2>(a, s);
   }
   if (w4 <= 16) return launch<8, 2, 4>(a, s);
   if (w4 <= 25) {   // w = 100 (products d0); variant 1: 6 groups x 5 lanes x 5 float4
@@ -488,7 +490,9 @@ digest_status spmm_one(const SpmmArgs& a, cudaStream_t s) {
     }
     if (v == 1) return launch<5, 5, 2, false>(a, s);
     if (v == 2) return launch<5, 5, 2, true>(a, s);
-    return launch<8, 4, 2, false, 4>(a, s);   // measured best for w=100 (9.2 ms, MB=4)
+    // measured best for w=100 with the persistent grid (products M=1): 7.75 ms vs 8.59 ms
+    // for <5,5,2,prefetch> and 10.2 ms for <5,5,2,rt> (profiles/r1_spmm_variant_sweep.log)
+    return launch<8, 4, 2, false, 4>(a, s);
   }
   if (w4 <= 32) return launch<8, 4, 2, false>(a, s);
   if (w4 <= 64) {

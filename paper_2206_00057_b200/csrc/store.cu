@@ -177,6 +177,46 @@ __global__ void k_put(const float* __restrict__ H, int64_t ldh, const int32_t* _
   if (dg::last_block_done(counter) && threadIdx.x == 0) dg::set_flags(sig);
 }
 
+// DIGEST-A snapshot pull (peer transport): CTA k copies owner segment k back -> front
+// under that owner's sequence word (seqlock: odd = a push is writing the segment).
+struct SnapSegs {
+  int64_t off[DIGEST_MAX_PARTS], cnt[DIGEST_MAX_PARTS];
+  const int64_t* seq[DIGEST_MAX_PARTS];
+};
+__global__ void __launch_bounds__(1024) k_snapshot(const float* back, float* front, int64_t ld,
+                                                   SnapSegs sg) {
+  __shared__ int64_t s1;
+  __shared__ int retry;
+  const int k = blockIdx.x;
+  const float4* src = reinterpret_cast<const float4*>(back + sg.off[k] * ld);
+  float4* dst = reinterpret_cast<float4*>(front + sg.off[k] * ld);
+  const int64_t n4 = sg.cnt[k] * ld / 4;
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    if (threadIdx.x == 0) {
+      int64_t v;
+      while ((v = dg::ld_acquire_sys(sg.seq[k])) & 1) __nanosleep(256);
+      s1 = v;
+    }
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < n4; i += blockDim.x) dst[i] = __ldcv(src + i);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      retry = dg::ld_acquire_sys(sg.seq[k]) != s1;
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (retry && t - t0 > 30ull * 1000000000ull) {
+        printf("digest: snapshot pull of segment %d never stabilised\n", k);
+        __trap();
+      }
+    }
+    __syncthreads();
+    if (!retry) break;
+  }
+}
+
 __global__ void k_copy(const float4* __restrict__ src, float4* __restrict__ dst, int64_t n4) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -349,23 +389,31 @@ digest_status digest_push_boundary(digest_store* st, int32_t level, const float*
   const bool peer = dg::is_peer(st->comm);
   if (peer) {
     DG_ARG(st->connected, DIGEST_E_STATE, "peer-transport store is not connected");
+    const bool nowait = (flags & DIGEST_PUSH_NOWAIT) != 0;
     Segs sg{};
     sg.nseg = M;
     dg::FlagWait wt{};
-    dg::FlagSet sig{};
+    dg::FlagSet sig{}, odd{};
     wt.value = L->last_pull;
-    sig.value = version;
+    sig.value = nowait ? 2 * version : version;
+    odd.value = 2 * version - 1;
     for (int k = 0; k < M; ++k) {
       sg.start[k] = p->send_off[k];
       sg.dst[k] = nullptr;
       if (k == me || p->send_count[k] == 0) continue;
       // same schedule on every rank => the receiver's back buffer has our index `back`
       sg.dst[k] = st->pl[k][level - 1].buf[back] + st->peer_recv_off[k][me] * L->ld;
-      wt.ptr[wt.n++] = dg::win_i64(st->comm->peer_win[k], dg::kWinPulled) + (level - 1);
+      if (!nowait)
+        wt.ptr[wt.n++] = dg::win_i64(st->comm->peer_win[k], dg::kWinPulled) + (level - 1);
       sig.ptr[sig.n++] = dg::win_i64(st->comm->peer_win[k], dg::kWinArrived) +
                          (int64_t)(level - 1) * 64 + me;
     }
     sg.start[M] = p->n_send;
+    if (nowait && p->n_send > 0) {   // seqlock: segment words odd while this push writes
+      for (int i = 0; i < sig.n; ++i) odd.ptr[i] = sig.ptr[i];
+      odd.n = sig.n;
+      DG_TRY(dg::flag_sync(dg::FlagWait{}, odd, s));
+    }
     if (p->n_send > 0) {
       int64_t blocks = dg::ceil_div(p->n_send, 8);
       int64_t cap = (int64_t)dg::num_sms() * 16;
@@ -432,8 +480,10 @@ digest_status digest_pull(digest_store* st, int32_t level, int64_t epoch, int32_
                           void* stream, const float** front_h) {
   Level* L;
   DG_TRY(get_level(st, level, &L));
-  DG_ARG(mode == DIGEST_PULL_FLIP || mode == DIGEST_PULL_COPY, DIGEST_E_INVALID, "bad pull mode");
+  DG_ARG(mode == DIGEST_PULL_FLIP || mode == DIGEST_PULL_COPY || mode == DIGEST_PULL_SNAPSHOT,
+         DIGEST_E_INVALID, "bad pull mode");
   cudaStream_t s = dg::as_stream(stream);
+  if (mode == DIGEST_PULL_SNAPSHOT && !dg::is_peer(st->comm)) mode = DIGEST_PULL_COPY;
   const int back = 1 - L->front;
   if (L->ver[back] >= epoch)
     return dg::set_error(DIGEST_E_STATE,
@@ -447,6 +497,26 @@ digest_status digest_pull(digest_store* st, int32_t level, int64_t epoch, int32_
     pulled.ptr[0] = dg::win_i64(st->comm->win, dg::kWinPulled) + (level - 1);
     pulled.value = epoch;
     L->last_pull = epoch;
+  }
+  if (peer && mode == DIGEST_PULL_SNAPSHOT) {   // DIGEST-A: no waiting for arrivals
+    if (L->ver[back] > L->ver[L->front]) {
+      const digest_part* p = st->part;
+      SnapSegs sg{};
+      int n = 0;
+      for (int k = 0; k < p->num_parts; ++k) {
+        if (k == p->rank || p->recv_count[k] == 0) continue;
+        sg.off[n] = p->recv_off[k];
+        sg.cnt[n] = p->recv_count[k];
+        sg.seq[n] = dg::win_i64(st->comm->win, dg::kWinArrived) + (int64_t)(level - 1) * 64 + k;
+        ++n;
+      }
+      if (n > 0)
+        DG_LAUNCH(DIGEST_PROF_PACK, s, 8.0 * st->part->n_halo * L->ld, 0, k_snapshot, n, 1024, 0,
+                  L->buf[back], L->buf[L->front], L->ld, sg);
+      L->ver[L->front] = L->ver[back];
+    }
+    if (front_h) *front_h = L->buf[L->front];
+    return DIGEST_OK;
   }
   if (L->ver[back] > L->ver[L->front]) {
     if (peer) {   // wait until every owner's rows of this version have arrived

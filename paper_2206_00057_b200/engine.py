@@ -38,6 +38,7 @@ class TrainConfig:
     cache_l1: bool = False      # aggregate the static layer-1 inputs once
     halo_grad: bool = False     # return P_out^T D W^T to the halo owners
     transport: str = "nccl"     # multi-process exchange: 'nccl' or 'peer' (CUDA IPC windows)
+    async_store: bool = False   # DIGEST-A on the peer transport: NOWAIT pushes, SNAPSHOT pulls
 
 
 class Partition:
@@ -158,7 +159,8 @@ class DigestWorker:
 
     def push(self, l, epoch, stream=None):
         cfg = self.cfg
-        flags = (D.PUSH_ASYNC if cfg.async_push else 0) | (D.PUSH_L2NORM if cfg.normalize_pushed else 0)
+        flags = ((D.PUSH_ASYNC if cfg.async_push else 0) | (D.PUSH_L2NORM if cfg.normalize_pushed else 0)
+                 | (D.PUSH_NOWAIT if cfg.async_store else 0))
         D.digest_push_boundary(self.store, l, self.H[l], epoch, flags, stream)
         self.pushes += 1
 
@@ -290,6 +292,21 @@ class AsyncLoopbackGroup:
     def close(self):
         for w in self.workers:
             w.close()
+
+
+def run_digest_a_peer(w, comm, epochs, alpha, delays_ns=None, stream=None):
+    """DIGEST-A for one rank of a multi-process run on the peer transport:
+    `epochs` local epochs of download (locked read of W_global in rank 0's window),
+    optional straggler delay (digest_delay), local epoch, upload (locked mixing).
+    No barrier and no AGG: ranks proceed at their own pace."""
+    if not (w.cfg.async_store and w.cfg.pull_mode == D.PULL_SNAPSHOT):
+        raise ValueError("DIGEST-A on the peer transport needs async_store and PULL_SNAPSHOT")
+    for r in range(1, epochs + 1):
+        D.digest_ps_download_peer(comm, w.W_flat, stream)
+        if delays_ns is not None and delays_ns[r - 1] > 0:
+            D.digest_delay(delays_ns[r - 1], stream)
+        w.local_epoch(r, stream)
+        D.digest_ps_upload_peer(comm, w.W_flat, alpha, stream)
 
 
 class LoopbackGroup:

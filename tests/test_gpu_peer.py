@@ -112,3 +112,53 @@ def test_peer_transport_multiprocess(name, tmp_path):
     lb_loss, lb_W = loopback(spec, cfg, inp, part)
     assert res["loss"].tobytes() == lb_loss.tobytes()
     assert W[0].tobytes() == lb_W.tobytes()
+
+
+ASYNC = {
+    "M1_equals_sync": dict(world=1, epochs=5, graph=dict(GRAPH, seed=31),
+                           train=dict(sync_interval=2, lr=0.05, optimizer="sgd")),
+    "M3_straggler": dict(world=3, epochs=6, graph=dict(GRAPH, seed=32), straggler=1,
+                         delay_ms=150.0, train=dict(sync_interval=1, lr=0.05, optimizer="sgd")),
+    "M4_adam_N2": dict(world=4, epochs=6, graph=dict(GRAPH, seed=33), straggler=3, delay_ms=50.0,
+                       train=dict(sync_interval=2, lr=0.01, optimizer="adam")),
+}
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("name", list(ASYNC))
+def test_digest_a_multiprocess(name, tmp_path):
+    """DIGEST-A over the peer transport: independent processes, locked PS
+    mixing in rank 0's window, NOWAIT pushes and seqlock SNAPSHOT pulls.  The order of
+    uploads is not reproducible, so the checks are the ones the method fixes: M*R PS
+    updates, one worker = the synchronous oracle, a straggler does not
+    hold the others back, finite weights that moved."""
+    import torch.multiprocessing as mp
+    from tests.peer_procs import run_rank_async
+    spec = ASYNC[name]
+    M, R = spec["world"], spec["epochs"]
+    out = str(tmp_path / "res.npz")
+    mp.start_processes(run_rank_async, args=(M, free_port(), spec, out), nprocs=M, join=True,
+                       start_method="spawn")
+    res = np.load(out)
+    assert int(res["updates"]) == M * R
+    Wg = res["W_global"]
+    cfg = small_config(**spec["graph"])
+    inp = make_inputs(cfg)
+    w0 = np.concatenate([w.ravel() for w in inp.weights])
+    assert np.isfinite(Wg).all() and np.isfinite(res["loss"]).all()
+    assert np.abs(Wg - w0).max() > 1e-4
+    tr = spec["train"]
+    if M == 1:
+        run = oracle.oracle_train(inp.indptr, inp.indices, inp.x, inp.y, inp.train_mask,
+                                  inp.weights, cfg.num_classes, np.zeros(cfg.num_nodes, np.int32),
+                                  1, sync_interval=tr["sync_interval"], epochs=R, lr=tr["lr"],
+                                  optimizer=tr["optimizer"])
+        for r, rec in enumerate(run.records):
+            assert abs(res["loss"][0][r] - rec.loss) <= TOL * abs(rec.loss)
+        assert rel(Wg, np.concatenate([w.ravel() for w in run.weights])) <= TOL
+    else:
+        s = spec["straggler"]
+        others = [m for m in range(M) if m != s]
+        # the others finish long before the straggler's injected delays have elapsed
+        assert res["wall"][others].max() < res["wall"][s] - 0.5 * R * spec["delay_ms"] / 1e3
+        assert res["loss"][:, -1].mean() < res["loss"][:, 0].mean()

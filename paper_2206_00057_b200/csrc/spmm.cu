@@ -120,7 +120,9 @@ __device__ __forceinline__ void spmm_row_epilogue(const SpmmArgs& a, int64_t row
 // starts and its first (col, val) chunk is loaded during the current row's last
 // gathers, so the row_ptr -> col -> gather dependency chain of a row overlaps the
 // previous row's gathers instead of following them (latency-bound narrow rows).
-template <int LC, int VPL, int UNR, bool XR, int MB>
+// H: per-gather L2 cache-policy operands (bit-31 hot rows evict_last); without them the
+// gathers are plain ld.global.nc (no per-load R2UR of a policy descriptor).
+template <int LC, int VPL, int UNR, bool XR, int MB, bool H = true>
 __global__ void __launch_bounds__(256, MB) k_spmm(SpmmArgs a) {
   constexpr int EG = 32 / LC;
   constexpr int STEP = EG * UNR;
@@ -209,7 +211,8 @@ __global__ void __launch_bounds__(256, MB) k_spmm(SpmmArgs a) {
 #pragma unroll
           for (int q = 0; q < VPL; ++q) {
             const int idx = cl + q * LC;
-            t[u][q] = (ok[u] && idx < w4) ? ld_gather(src[u] + 4 * idx, pol[u])
+            t[u][q] = (ok[u] && idx < w4) ? (H ? ld_gather(src[u] + 4 * idx, pol[u])
+                                                 : ldg4(src[u] + 4 * idx))
                                           : make_float4(0.f, 0.f, 0.f, 0.f);
           }
         if (XR && st == 0 && last) next_row_chunk();
@@ -369,11 +372,26 @@ bool spmm_persistent(const SpmmArgs& a) {
 template <int LC, int VPL, int UNR, bool PF, int MB>
 digest_status launch_mb(const SpmmArgs& a, cudaStream_t s, int64_t blocks, double bytes,
                         double flops) {
-  if (PF) {
-    static const int64_t cap = resident_ctas(k_spmm<LC, VPL, UNR, false, MB>);
+  // DIGEST_SPMM_PFH=1: cache-policy operands in the prefetching (narrow-width) kernel.
+  // Off by default: the per-load policy descriptor costs an R2UR per gather in this
+  // instruction-bound kernel (w=48 products M=1: 4.12 -> 3.85 ms without, M=8: 0.515 ->
+  // 0.454 ms; profiles/r1_spmm_variant_sweep.log)
+  static int pfh = -1;
+  if (pfh < 0) {
+    const char* e = getenv("DIGEST_SPMM_PFH");
+    pfh = e ? atoi(e) : 0;
+  }
+  if (PF && pfh && a.hints) {
+    static const int64_t cap = resident_ctas(k_spmm<LC, VPL, UNR, false, MB, true>);
     if (spmm_persistent(a) && blocks > cap) blocks = cap;
     DG_LAUNCH_TAG(DIGEST_PROF_SPMM, a.full_width > 0 ? a.full_width : a.width, s, bytes, flops,
-                  (k_spmm<LC, VPL, UNR, false, MB>),
+                  (k_spmm<LC, VPL, UNR, false, MB, true>),
+                  (unsigned)blocks, 256, 0, a);
+  } else if (PF) {
+    static const int64_t cap = resident_ctas(k_spmm<LC, VPL, UNR, false, MB, false>);
+    if (spmm_persistent(a) && blocks > cap) blocks = cap;
+    DG_LAUNCH_TAG(DIGEST_PROF_SPMM, a.full_width > 0 ? a.full_width : a.width, s, bytes, flops,
+                  (k_spmm<LC, VPL, UNR, false, MB, false>),
                   (unsigned)blocks, 256, 0, a);
   } else {
     static const int64_t cap = resident_ctas(k_spmm_rt<LC, VPL, UNR, MB>);
@@ -479,7 +497,7 @@ digest_status spmm_one(const SpmmArgs& a, cudaStream_t s) {
     if (v == 4) return launch<8, 2, 2>(a, s);
     // measured best for w=48 with the persistent grid (products M=1): 4.11 ms vs 4.30 ms
     // for <4,3,4> (profiles/r1_spmm_variant_sweep.log)
-    return launch<4, 3, 2>(a, s);
+    return launch<4, 3, 2, true, 4>(a, s);
   }
   if (w4 <= 16) return launch<8, 2, 4>(a, s);
   if (w4 <= 25) {   // w = 100 (products d0); variant 1: 6 groups x 5 lanes x 5 float4

@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--share-gpu", action="store_true",
                     help="testing only: every rank on cuda:0, gloo process group (timings are "
                          "time-sliced, not a scaling number)")
+    ap.add_argument("--loopback", type=int, default=0,
+                    help="N=1 only: train M partitions in one process on one GPU (linked stores, "
+                         "the sync-interval / exchange-cost sweep); the step covers all M parts")
     ap.add_argument("--cache-l1", action="store_true",
                     help="aggregate the static layer-1 inputs once (SURVEY f3 (i)); off by default")
     return ap.parse_args()
@@ -185,6 +188,10 @@ def run_ours(a, rank, world, local):
 
     cfg = get_config(a.config)
     M = world
+    loop = a.loopback > 1 and world == 1
+    if loop:
+        M = a.loopback
+        a.no_e2e = True
     t0 = time.time()
     inp = make_inputs(cfg)
     part_of = make_block_parts(cfg, M)
@@ -205,8 +212,16 @@ def run_ours(a, rank, world, local):
                      lr=0.01, optimizer="adam", async_push=(a.mode == "async"),
                      cache_l1=a.cache_l1, fresh=a.fresh, transport=a.transport)
     t1 = time.time()
-    (w,) = build_workers(inp.indptr, inp.indices, inp.x, inp.y, inp.train_mask, inp.weights,
-                         part_of, M, tc, ranks=[rank], comm_grad=comm_grad, comm_halo=comm_halo)
+    if loop:
+        from paper_2206_00057_b200.engine import LoopbackGroup
+        ws = build_workers(inp.indptr, inp.indices, inp.x, inp.y, inp.train_mask, inp.weights,
+                           part_of, M, tc)
+        grp = LoopbackGroup(ws)
+        w = ws[0]
+    else:
+        (w,) = build_workers(inp.indptr, inp.indices, inp.x, inp.y, inp.train_mask, inp.weights,
+                             part_of, M, tc, ranks=[rank], comm_grad=comm_grad, comm_halo=comm_halo)
+        grp = w
     torch.cuda.synchronize()
     t_part = time.time() - t1
     info = w.part.info
@@ -230,7 +245,7 @@ def run_ours(a, rank, world, local):
     r = 0
     for _ in range(a.warmup):
         r += 1
-        w.epoch(r)
+        grp.epoch(r)
     barrier()
 
     # ---- timed region (device time, CUDA events on the launching stream)
@@ -243,7 +258,7 @@ def run_ours(a, rank, world, local):
     e0.record(stream)
     for _ in range(a.steps):
         r += 1
-        w.epoch(r)
+        grp.epoch(r)
     e1.record(stream)
     barrier()
     launches = D.digest_launch_count() - n0
@@ -299,7 +314,7 @@ def run_ours(a, rank, world, local):
         nz = sum(d["flops"] / (2.0 * d["tag"]) for d in detail if d["cls"] == "spmm" and d["tag"])
         gteps = nz / (spmm["ms"] / 1e3) / 1e9
     cpu = None
-    if rank == 0 and world == 1:   # the oracle baseline is timed at N=1 only
+    if rank == 0 and world == 1 and not loop:   # the oracle baseline is timed at N=1 only
         per, sample = oracle_sample_epoch_seconds(a.config, M, a.sample_frac, 1, 1)
         cpu = {"value": float(np.mean(per)), "unit": "s", "cores": cores(), "kind": "oracle",
                "sample": sample}
@@ -311,6 +326,7 @@ def run_ours(a, rank, world, local):
             "config": {"workload": a.config, "num_nodes": cfg.num_nodes, "nnz": cfg.nnz,
                        "parts": M, "dims": list(cfg.dims), "sync_interval": n_sync,
                        "fresh": a.fresh, "transport": a.transport if world > 1 else None,
+                       "loopback_parts_on_one_gpu": M if loop else None,
                        "mode": a.mode, "cache_l1": a.cache_l1,
                        "n_local": info.n_local, "n_halo": info.n_halo,
                        "nnz_local": info.nnz, "l2": "inputs larger than L2 (no flush needed)"},
@@ -330,7 +346,7 @@ def run_ours(a, rank, world, local):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()      # no rank unmaps a buffer a peer may still read
-    w.close()
+    grp.close()
     if world > 1:
         D.digest_comm_destroy(comm_grad)
         if comm_halo != comm_grad:

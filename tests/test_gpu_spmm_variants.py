@@ -1,0 +1,45 @@
+"""Every SpMM kernel variant the library can select (environment switches, one fresh
+process each) vs the oracle's fp64 P_m X_ext (Eq. 5) on a graph with rows of
+0..~200 nonzeros (several 32-pair chunks and ragged tails), a random 3-way partition
+(halo columns through the second source pointer) and widths that exercise every lane
+layout.  Bar: 1e-4 relative (north_star)."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from oracle.gcn import layer_forward
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CASES = [(48, {"DIGEST_SPMM_V12": str(v)}) for v in range(5)]
+CASES += [(48, {"DIGEST_SPMM_PFH": "1"}), (48, {"DIGEST_SPMM_GRID": "1"})]
+CASES += [(100, {"DIGEST_SPMM_V25": str(v)}) for v in range(3)]
+CASES += [(256, {"DIGEST_SPMM_V": str(v)}) for v in range(6)]
+CASES += [(256, {"DIGEST_SPMM_SLAB": "64"}), (256, {"DIGEST_SPMM_HINTS": "0"}),
+          (256, {"DIGEST_SPMM_GRID": "0"}), (100, {"DIGEST_SPMM_SLAB": "32"})]
+CASES += [(w, {}) for w in (4, 8, 16, 32, 64, 128, 384, 512, 1024)]
+CASES += [(w, {"DIGEST_SPMM_MB": mb}) for w in (48, 100, 256) for mb in ("4", "6")]
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("width,env", CASES, ids=[f"w{w}-" + "-".join(f"{k[12:]}{v}" for k, v in e.items())
+                                                  for w, e in CASES])
+def test_spmm_variant(width, env, tmp_path):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    out = str(tmp_path / "y.npz")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "spmm_variant_proc.py"), out,
+                        str(width), "5"], env={**os.environ, **env, "PYTHONPATH": ROOT},
+                       capture_output=True, text=True, timeout=280)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = np.load(out)
+    op = oracle.oracle_partition(d["ip"], d["ix"], d["part"], 3, 1)
+    ref = layer_forward(op, d["xl"], d["xh"], np.eye(width), relu=False)["A"]
+    err = np.abs(d["y"] - ref).max() / np.abs(ref).max()
+    assert err <= 1e-4, err

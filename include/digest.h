@@ -165,6 +165,16 @@ enum { DIGEST_PULL_FLIP = 0, DIGEST_PULL_COPY = 1, DIGEST_PULL_SNAPSHOT = 2 };
 digest_status digest_store_create(const digest_part* part, digest_comm* comm,
                                   int32_t num_levels, const int32_t* width_h,
                                   digest_store** out_h);
+/* The same with flags.  DIGEST_STORE_BF16: the back buffers, the send
+ * buffers and every transfer (loopback, NCCL, peer) hold bf16 copies of the pushed rows
+ * (round to nearest even), half the exchange bytes; the front buffer stays fp32 and a
+ * pull widens back -> front exactly (FLIP pulls become this copy).  The halo inputs then
+ * carry bf16 precision (relative 2^-9), so parity with the oracle holds only with the
+ * oracle's matching store_dtype='bf16' and a looser tolerance. */
+enum { DIGEST_STORE_BF16 = 1u };
+digest_status digest_store_create_ex(const digest_part* part, digest_comm* comm,
+                                     int32_t num_levels, const int32_t* width_h, uint32_t flags,
+                                     digest_store** out_h);
 /* Link the stores of all partitions of one process, index = rank (loopback). */
 digest_status digest_store_link(digest_store* const* stores_h, int32_t count);
 /* north_star call #4 ("push", Alg. 1 PUSH P:220-221).  Packs the boundary

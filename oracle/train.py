@@ -18,6 +18,9 @@ Schedule, Alg. 1, 1-based epochs r, levels l in [1, L-1] only
     (Eq. 3 P:100 with the (1/M) sum of P:702).
   * mode 'fresh' (reading A15, a test hook): after every part computed
     level l, halo^(l,m) is set to the CURRENT epoch's values (zero staleness).
+  * store_dtype 'bf16': the store keeps the pushed rows rounded to
+    bfloat16 (fp32 first, then round-to-nearest-even to 8 significant bits), so the
+    pulled halo rows carry that rounding.
 """
 from dataclasses import dataclass, field
 import numpy as np
@@ -25,6 +28,15 @@ import scipy.sparse as sp
 
 from .partition import oracle_partition
 from .gcn import layer_forward, layer_backward, cross_entropy, sgd_step, adam_step, normalize_rows
+
+
+def bf16_round(x):
+    """fp64 -> fp32 (RNE) -> bfloat16 (RNE on the top 16 bits of the fp32 pattern), as fp64.
+    Finite inputs only (the store never holds NaN/Inf)."""
+    f = np.ascontiguousarray(np.asarray(x, np.float32)).view(np.uint32).astype(np.uint64)
+    lsb = (f >> 16) & 1
+    r = ((f + 0x7FFF + lsb) & 0xFFFF0000).astype(np.uint32)
+    return r.view(np.float32).astype(np.float64)
 
 
 # ---------------------------------------------------------------- full graph (O12 i)
@@ -94,12 +106,15 @@ def oracle_train(indptr, indices, x, y, train_mask, weights, num_classes, part_o
                  num_parts, sync_interval, epochs, lr=0.01, optimizer="sgd",
                  cold_start="zero", mode="stale", normalize_pushed=False,
                  loss_weighting="count", record_outputs=False, parts=None,
-                 halo_grad="none") -> OracleRun:
+                 halo_grad="none", store_dtype="fp32") -> OracleRun:
     """halo_grad: 'none' (halo inputs are constants, P:810 -- the default) or
     'same_epoch' (the appendix's P_out^T D W^T term, computed by each
     part for its halo rows and returned to the owners in the same iteration)."""
     if halo_grad not in ("none", "same_epoch"):
         raise ValueError(halo_grad)
+    if store_dtype not in ("fp32", "bf16"):
+        raise ValueError(store_dtype)
+    store = bf16_round if store_dtype == "bf16" else (lambda v: v)
     if sync_interval < 1 or epochs < 1:
         raise ValueError("sync interval and epochs must be >= 1")
     M, Ns = num_parts, sync_interval
@@ -161,7 +176,7 @@ def oracle_train(indptr, indices, x, y, train_mask, weights, num_classes, part_o
                 break
             if mode == "fresh":
                 for m, p in enumerate(parts):
-                    halo[(l, m)] = glob[p.halo_ids].copy()
+                    halo[(l, m)] = store(glob[p.halo_ids])
                     halo_ver[(l, m)] = np.full(p.n_halo, r, np.int64)
             rec.eps[l] = max([float(np.sqrt(((halo[(l, m)] - glob[p.halo_ids]) ** 2).sum(1)).max())
                               if p.n_halo else 0.0 for m, p in enumerate(parts)])
@@ -172,7 +187,7 @@ def oracle_train(indptr, indices, x, y, train_mask, weights, num_classes, part_o
                 loc_in[m] = outs[(l, m)]["H"]
                 halo_in[m] = halo[(l, m)]
             if push:
-                pending[l] = normalize_rows(glob) if normalize_pushed else glob
+                pending[l] = store(normalize_rows(glob) if normalize_pushed else glob)
                 run.push_count += M
             rec.reps[l] = glob
         # loss, backward (layer-major over the parts), AGG, update

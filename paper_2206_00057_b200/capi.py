@@ -19,6 +19,7 @@ ORDER_AUTO, ORDER_AGG_FIRST, ORDER_XFORM_FIRST = 0, 1, 2
 PUSH_ASYNC, PUSH_L2NORM, PUSH_NOWAIT = 1, 2, 4
 PULL_FLIP, PULL_COPY, PULL_SNAPSHOT = 0, 1, 2
 IPC_HANDLE_BYTES = 64
+STORE_BF16 = 1
 PROF_SPMM, PROF_GEMM, PROF_PACK, PROF_OTHER = 0, 1, 2, 3
 STATUS = {0: "OK", 1: "E_INVALID", 2: "E_SHAPE", 3: "E_STATE", 4: "E_CUDA", 5: "E_NCCL",
           6: "E_NOMEM", 7: "E_UNSUPPORTED"}
@@ -65,6 +66,7 @@ _SIGS = {
     "digest_part_export": ([_p] * 11, _i32),
     "digest_part_destroy": ([_p], _i32),
     "digest_store_create": ([_p, _p, _i32, _p, _p], _i32),
+    "digest_store_create_ex": ([_p, _p, _i32, _p, _u32, _p], _i32),
     "digest_store_link": ([_p, _i32], _i32),
     "digest_push_boundary": ([_p, _i32, _p, _i64, _i64, _u32, _p], _i32),
     "digest_pull": ([_p, _i32, _i64, _i32, _p, _p], _i32),
@@ -232,7 +234,16 @@ def digest_part_destroy(part):
 
 
 # ------------------------------------------------------------------ store
-def digest_store_create(part, comm, widths):
+def digest_store_create_ex(part, comm, widths, flags=0):
+    arr = (C.c_int32 * max(1, len(widths)))(*widths)
+    out = C.c_void_p()
+    _check(lib.digest_store_create_ex(part, comm, len(widths), arr, flags, C.byref(out)))
+    return out.value
+
+
+def digest_store_create(part, comm, widths, flags=0):
+    if flags:
+        return digest_store_create_ex(part, comm, widths, flags)
     arr = (C.c_int32 * max(1, len(widths)))(*widths)
     out = C.c_void_p()
     _check(lib.digest_store_create(part, comm, len(widths), arr, C.byref(out)))

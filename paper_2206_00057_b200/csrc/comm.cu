@@ -23,19 +23,20 @@ digest_status comm_allreduce_sum(digest_comm* c, float* buf, int64_t count, cuda
 }
 
 digest_status comm_alltoallv(digest_comm* c, const float* const* send, const int64_t* count_s,
-                             float* const* recv, const int64_t* count_r, cudaStream_t s) {
+                             float* const* recv, const int64_t* count_r, cudaStream_t s,
+                             ncclDataType_t dt) {
   DG_NCCL(ncclGroupStart());
   for (int k = 0; k < c->nranks; ++k) {
     if (k == c->rank) continue;
     if (count_s[k] > 0) {
-      ncclResult_t r = ncclSend(send[k], (size_t)count_s[k], ncclFloat, k, c->comm, s);
+      ncclResult_t r = ncclSend(send[k], (size_t)count_s[k], dt, k, c->comm, s);
       if (r != ncclSuccess) {
         ncclGroupEnd();
         return set_error(DIGEST_E_NCCL, "ncclSend: %s", ncclGetErrorString(r));
       }
     }
     if (count_r[k] > 0) {
-      ncclResult_t r = ncclRecv(recv[k], (size_t)count_r[k], ncclFloat, k, c->comm, s);
+      ncclResult_t r = ncclRecv(recv[k], (size_t)count_r[k], dt, k, c->comm, s);
       if (r != ncclSuccess) {
         ncclGroupEnd();
         return set_error(DIGEST_E_NCCL, "ncclRecv: %s", ncclGetErrorString(r));

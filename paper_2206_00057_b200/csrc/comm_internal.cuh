@@ -36,7 +36,8 @@ digest_status comm_allreduce_sum(digest_comm* c, float* buf, int64_t count, cuda
 // Grouped point-to-point all-to-allv: send[k] (count_s[k] floats) to rank k and
 // recv[k] (count_r[k] floats) from rank k, k != own rank.
 digest_status comm_alltoallv(digest_comm* c, const float* const* send, const int64_t* count_s,
-                             float* const* recv, const int64_t* count_r, cudaStream_t s);
+                             float* const* recv, const int64_t* count_r, cudaStream_t s,
+                             ncclDataType_t dt = ncclFloat);
 inline bool is_peer(const digest_comm* c) { return c && c->kind == 1 && c->nranks > 1; }
 inline bool is_nccl(const digest_comm* c) { return c && c->kind == 0 && c->nranks > 1; }
 inline int64_t* win_i64(char* w, size_t off) { return reinterpret_cast<int64_t*>(w + off); }

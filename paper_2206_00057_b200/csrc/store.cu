@@ -13,6 +13,8 @@
 //     (async mode, overlapping the next layer: P:250-251).
 // A pull flips front/back (or copies, CUDA-graph safe) only when the back buffer
 // holds a newer version that is older than the current epoch (reading A7).
+#include <cuda_bf16.h>
+
 #include <cstring>
 #include <vector>
 
@@ -25,7 +27,7 @@ namespace {
 struct Level {
   int32_t width = 0;
   int64_t ld = 0;
-  float* buf[2] = {nullptr, nullptr};
+  float* buf[2] = {nullptr, nullptr};   // bf16 store: buf[0] fp32 front, buf[1] bf16 back
   int64_t ver[2] = {0, 0};
   int front = 0;
   float* send_buf = nullptr;
@@ -36,8 +38,38 @@ struct Level {
   float* ret_recv = nullptr;    // n_send x ld: returned gradients received from peers (NCCL)
   int64_t last_pull = 0;        // epoch of the last pull call (peer transport)
   int64_t gseq = 0;             // grad_buffer calls so far (peer transport)
-  size_t halo_bytes = 0;        // bytes of one n_halo x ld buffer
+  size_t halo_bytes = 0;        // bytes of one n_halo x ld fp32 buffer
+  bool bf16 = false;            // back buffer (and transfers) in bf16
+  size_t es() const { return bf16 ? 2 : 4; }   // element size of back / send buffers
 };
+
+// Row `row` of a back/send buffer with leading dimension ld and element size es.
+__host__ __device__ inline float* xrow(float* base, int64_t row, int64_t ld, size_t es) {
+  return reinterpret_cast<float*>(reinterpret_cast<char*>(base) + (size_t)row * ld * es);
+}
+
+// Store 4 consecutive values at float4 column c of a row, as fp32 or as bf16 (RNE).
+template <bool BF>
+__device__ __forceinline__ void st4(float* row, int c, float4 v) {
+  if (BF) {
+    __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&a);
+    u.y = *reinterpret_cast<uint32_t*>(&b);
+    reinterpret_cast<uint2*>(row)[c] = u;
+  } else {
+    reinterpret_cast<float4*>(row)[c] = v;
+  }
+}
+template <bool BF>
+__device__ __forceinline__ float4 ld4(const float* row, int c) {
+  if (BF) {
+    const uint2 u = __ldcv(reinterpret_cast<const uint2*>(row) + c);
+    return make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xffff0000u),
+                       __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xffff0000u));
+  }
+  return __ldcv(reinterpret_cast<const float4*>(row) + c);
+}
 
 // What a peer needs to reach this store's buffers (digest_store_export / _connect).
 struct PeerBlob {
@@ -92,7 +124,7 @@ struct Segs {
 
 // Row s of the send list -> segment k (binary search), destination row s - start[k].
 // Optional row L2 normalisation (Alg. 1, applied to the pushed copies only).
-template <bool NORM>
+template <bool NORM, bool BF>
 __global__ void k_pack(const float* __restrict__ H, int64_t ldh, const int32_t* __restrict__ idx,
                        int64_t n_send, Segs segs, int64_t ld, int w4) {
   const int lane = threadIdx.x & 31;
@@ -105,7 +137,7 @@ __global__ void k_pack(const float* __restrict__ H, int64_t ldh, const int32_t* 
       if (segs.start[mid] <= r) lo = mid; else hi = mid - 1;
     }
     const float4* src = reinterpret_cast<const float4*>(H + (int64_t)idx[r] * ldh);
-    float4* dst = reinterpret_cast<float4*>(segs.dst[lo] + (r - segs.start[lo]) * ld);
+    float* dst = xrow(segs.dst[lo], r - segs.start[lo], ld, BF ? 2 : 4);
     float scale = 1.f;
     if (NORM) {
       float ss = 0.f;
@@ -125,7 +157,7 @@ __global__ void k_pack(const float* __restrict__ H, int64_t ldh, const int32_t* 
         v.z *= scale;
         v.w *= scale;
       }
-      dst[c] = v;
+      st4<BF>(dst, c, v);
     }
   }
 }
@@ -135,7 +167,7 @@ __global__ void k_pack(const float* __restrict__ H, int64_t ldh, const int32_t* 
 // (its `pulled` flag), then writes its rows straight into the peers' back buffers
 // through their IPC mappings; the last block to finish fences and raises the
 // receivers' `arrived` flags to the pushed version.
-template <bool NORM>
+template <bool NORM, bool BF>
 __global__ void k_put(const float* __restrict__ H, int64_t ldh, const int32_t* __restrict__ idx,
                       int64_t n_send, Segs segs, int64_t ld, int w4, dg::FlagWait wait,
                       dg::FlagSet sig, unsigned* counter) {
@@ -151,7 +183,7 @@ __global__ void k_put(const float* __restrict__ H, int64_t ldh, const int32_t* _
       if (segs.start[mid] <= r) lo = mid; else hi = mid - 1;
     }
     const float4* src = reinterpret_cast<const float4*>(H + (int64_t)idx[r] * ldh);
-    float4* dst = reinterpret_cast<float4*>(segs.dst[lo] + (r - segs.start[lo]) * ld);
+    float* dst = xrow(segs.dst[lo], r - segs.start[lo], ld, BF ? 2 : 4);
     float scale = 1.f;
     if (NORM) {
       float ss = 0.f;
@@ -171,7 +203,7 @@ __global__ void k_put(const float* __restrict__ H, int64_t ldh, const int32_t* _
         v.z *= scale;
         v.w *= scale;
       }
-      dst[c] = v;
+      st4<BF>(dst, c, v);
     }
   }
   if (dg::last_block_done(counter) && threadIdx.x == 0) dg::set_flags(sig);
@@ -183,12 +215,13 @@ struct SnapSegs {
   int64_t off[DIGEST_MAX_PARTS], cnt[DIGEST_MAX_PARTS];
   const int64_t* seq[DIGEST_MAX_PARTS];
 };
+template <bool BF>
 __global__ void __launch_bounds__(1024) k_snapshot(const float* back, float* front, int64_t ld,
                                                    SnapSegs sg) {
   __shared__ int64_t s1;
   __shared__ int retry;
   const int k = blockIdx.x;
-  const float4* src = reinterpret_cast<const float4*>(back + sg.off[k] * ld);
+  const float* src = xrow(const_cast<float*>(back), sg.off[k], ld, BF ? 2 : 4);
   float4* dst = reinterpret_cast<float4*>(front + sg.off[k] * ld);
   const int64_t n4 = sg.cnt[k] * ld / 4;
   uint64_t t0;
@@ -200,7 +233,7 @@ __global__ void __launch_bounds__(1024) k_snapshot(const float* back, float* fro
       s1 = v;
     }
     __syncthreads();
-    for (int64_t i = threadIdx.x; i < n4; i += blockDim.x) dst[i] = __ldcv(src + i);
+    for (int64_t i = threadIdx.x; i < n4; i += blockDim.x) dst[i] = ld4<BF>(src, (int)i);
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -215,6 +248,13 @@ __global__ void __launch_bounds__(1024) k_snapshot(const float* back, float* fro
     __syncthreads();
     if (!retry) break;
   }
+}
+
+// bf16 store pull: front (fp32) <- back (bf16), exact widening.
+__global__ void k_widen(const float* __restrict__ src, float4* __restrict__ dst, int64_t n4) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = ld4<true>(src, (int)i);
 }
 
 __global__ void k_copy(const float4* __restrict__ src, float4* __restrict__ dst, int64_t n4) {
@@ -277,18 +317,20 @@ digest_status get_level(digest_store* st, int32_t level, Level** out) {
 }
 
 digest_status pack(const float* H, int64_t ldh, const int32_t* idx, int64_t n_send, const Segs& sg,
-                   int64_t ld, int32_t width, bool norm, cudaStream_t s) {
+                   int64_t ld, int32_t width, bool norm, cudaStream_t s, bool bf = false) {
   if (n_send == 0) return DIGEST_OK;
   int64_t blocks = dg::ceil_div(n_send, 8);
   int64_t cap = (int64_t)dg::num_sms() * 16;
   if (blocks > cap) blocks = cap;
-  double bytes = (double)n_send * (8.0 * width + 4.0);
-  if (norm)
-    DG_LAUNCH(DIGEST_PROF_PACK, s, bytes, 0, k_pack<true>, (unsigned)blocks, 256, 0, H, ldh, idx,
-              n_send, sg, ld, width / 4);
-  else
-    DG_LAUNCH(DIGEST_PROF_PACK, s, bytes, 0, k_pack<false>, (unsigned)blocks, 256, 0, H, ldh, idx,
-              n_send, sg, ld, width / 4);
+  double bytes = (double)n_send * ((bf ? 6.0 : 8.0) * width + 4.0);
+#define DG_PACK(NORM, BF)                                                                        \
+  DG_LAUNCH(DIGEST_PROF_PACK, s, bytes, 0, (k_pack<NORM, BF>), (unsigned)blocks, 256, 0, H, ldh, \
+            idx, n_send, sg, ld, width / 4)
+  if (norm && bf) DG_PACK(true, true);
+  else if (norm) DG_PACK(true, false);
+  else if (bf) DG_PACK(false, true);
+  else DG_PACK(false, false);
+#undef DG_PACK
   return DIGEST_OK;
 }
 
@@ -298,6 +340,13 @@ extern "C" {
 
 digest_status digest_store_create(const digest_part* part, digest_comm* comm, int32_t num_levels,
                                   const int32_t* width_h, digest_store** out_h) {
+  return digest_store_create_ex(part, comm, num_levels, width_h, 0u, out_h);
+}
+
+digest_status digest_store_create_ex(const digest_part* part, digest_comm* comm,
+                                     int32_t num_levels, const int32_t* width_h, uint32_t flags,
+                                     digest_store** out_h) {
+  DG_ARG((flags & ~DIGEST_STORE_BF16) == 0, DIGEST_E_INVALID, "unknown store flags 0x%x", flags);
   DG_ARG(part && out_h, DIGEST_E_INVALID, "NULL argument");
   DG_ARG(num_levels >= 0 && num_levels <= 64 && (num_levels == 0 || width_h), DIGEST_E_INVALID,
          "bad level list");
@@ -323,12 +372,14 @@ digest_status digest_store_create(const digest_part* part, digest_comm* comm, in
     }
     L.width = width_h[l];
     L.ld = dg::round_up(L.width, 4);
+    L.bf16 = (flags & DIGEST_STORE_BF16) != 0;
     size_t hb = sizeof(float) * (size_t)(part->n_halo > 0 ? part->n_halo : 1) * L.ld;
-    size_t sb = sizeof(float) * (size_t)(part->n_send > 0 ? part->n_send : 1) * L.ld;
+    size_t sb = L.es() * (size_t)(part->n_send > 0 ? part->n_send : 1) * L.ld;
     for (int b = 0; b < 2; ++b) {
-      if (cudaMalloc(&L.buf[b], hb) != cudaSuccess)
+      const size_t bytes = (b == 1 && L.bf16) ? hb / 2 : hb;   // bf16: buf[1] is the back buffer
+      if (cudaMalloc(&L.buf[b], bytes) != cudaSuccess)
         return fail(dg::set_error(DIGEST_E_NOMEM, "halo buffer allocation failed"));
-      if (cudaMemset(L.buf[b], 0, hb) != cudaSuccess)
+      if (cudaMemset(L.buf[b], 0, bytes) != cudaSuccess)
         return fail(dg::set_error(DIGEST_E_CUDA, "cudaMemset failed"));
     }
     L.halo_bytes = hb;
@@ -337,7 +388,9 @@ digest_status digest_store_create(const digest_part* part, digest_comm* comm, in
         cudaMemset(L.grad_buf, 0, gb) != cudaSuccess)
       return fail(dg::set_error(DIGEST_E_NOMEM, "gradient-return buffer allocation failed"));
     if (dg::is_nccl(comm)) {
-      if (cudaMalloc(&L.send_buf, sb) != cudaSuccess || cudaMalloc(&L.ret_recv, sb) != cudaSuccess)
+      if (cudaMalloc(&L.send_buf, sb) != cudaSuccess ||
+          cudaMalloc(&L.ret_recv, sizeof(float) * (size_t)(part->n_send > 0 ? part->n_send : 1) *
+                                      L.ld) != cudaSuccess)
         return fail(dg::set_error(DIGEST_E_NOMEM, "send buffer allocation failed"));
     }
     if (cudaEventCreateWithFlags(&L.done, cudaEventDisableTiming) != cudaSuccess)
@@ -402,7 +455,7 @@ digest_status digest_push_boundary(digest_store* st, int32_t level, const float*
       sg.dst[k] = nullptr;
       if (k == me || p->send_count[k] == 0) continue;
       // same schedule on every rank => the receiver's back buffer has our index `back`
-      sg.dst[k] = st->pl[k][level - 1].buf[back] + st->peer_recv_off[k][me] * L->ld;
+      sg.dst[k] = xrow(st->pl[k][level - 1].buf[back], st->peer_recv_off[k][me], L->ld, L->es());
       if (!nowait)
         wt.ptr[wt.n++] = dg::win_i64(st->comm->peer_win[k], dg::kWinPulled) + (level - 1);
       sig.ptr[sig.n++] = dg::win_i64(st->comm->peer_win[k], dg::kWinArrived) +
@@ -418,15 +471,16 @@ digest_status digest_push_boundary(digest_store* st, int32_t level, const float*
       int64_t blocks = dg::ceil_div(p->n_send, 8);
       int64_t cap = (int64_t)dg::num_sms() * 16;
       if (blocks > cap) blocks = cap;
-      double bytes = (double)p->n_send * (8.0 * L->width + 4.0);
-      if (norm)
-        DG_LAUNCH(DIGEST_PROF_PACK, s, bytes, 0, k_put<true>, (unsigned)blocks, 256, 0, H_local, ld,
-                  p->send_idx, p->n_send, sg, L->ld, L->width / 4, wt, sig,
-                  st->counters + (level - 1));
-      else
-        DG_LAUNCH(DIGEST_PROF_PACK, s, bytes, 0, k_put<false>, (unsigned)blocks, 256, 0, H_local,
-                  ld, p->send_idx, p->n_send, sg, L->ld, L->width / 4, wt, sig,
-                  st->counters + (level - 1));
+      double bytes = (double)p->n_send * ((4.0 + L->es()) * L->width + 4.0);
+#define DG_PUT(NORM, BF)                                                                      \
+  DG_LAUNCH(DIGEST_PROF_PACK, s, bytes, 0, (k_put<NORM, BF>), (unsigned)blocks, 256, 0, H_local, \
+            ld, p->send_idx, p->n_send, sg, L->ld, L->width / 4, wt, sig,                      \
+            st->counters + (level - 1))
+      if (norm && L->bf16) DG_PUT(true, true);
+      else if (norm) DG_PUT(true, false);
+      else if (L->bf16) DG_PUT(false, true);
+      else DG_PUT(false, false);
+#undef DG_PUT
     }
   } else if (M > 1 && !nccl) {
     DG_ARG((int)st->peers.size() == M, DIGEST_E_STATE,
@@ -441,10 +495,11 @@ digest_status digest_push_boundary(digest_store* st, int32_t level, const float*
       }
       digest_store* pk = st->peers[k];
       Level& Lk = pk->lev[level - 1];
-      sg.dst[k] = Lk.buf[1 - Lk.front] + pk->part->recv_off[me] * Lk.ld;
+      DG_ARG(Lk.bf16 == L->bf16, DIGEST_E_STATE, "linked stores disagree on the bf16 store");
+      sg.dst[k] = xrow(Lk.buf[1 - Lk.front], pk->part->recv_off[me], Lk.ld, Lk.es());
     }
     sg.start[M] = p->n_send;
-    DG_TRY(pack(H_local, ld, p->send_idx, p->n_send, sg, L->ld, L->width, norm, s));
+    DG_TRY(pack(H_local, ld, p->send_idx, p->n_send, sg, L->ld, L->width, norm, s, L->bf16));
   } else if (nccl) {
     if (L->inflight) DG_CUDA(cudaStreamWaitEvent(s, L->done, 0));  // send buffer reuse
     Segs sg{};
@@ -452,13 +507,13 @@ digest_status digest_push_boundary(digest_store* st, int32_t level, const float*
     sg.dst[0] = L->send_buf;
     sg.start[0] = 0;
     sg.start[1] = p->n_send;
-    DG_TRY(pack(H_local, ld, p->send_idx, p->n_send, sg, L->ld, L->width, norm, s));
+    DG_TRY(pack(H_local, ld, p->send_idx, p->n_send, sg, L->ld, L->width, norm, s, L->bf16));
     std::vector<const float*> sp(M);
     std::vector<float*> rp(M);
     std::vector<int64_t> cs(M), cr(M);
     for (int k = 0; k < M; ++k) {
-      sp[k] = L->send_buf + p->send_off[k] * L->ld;
-      rp[k] = L->buf[back] + p->recv_off[k] * L->ld;
+      sp[k] = xrow(L->send_buf, p->send_off[k], L->ld, L->es());
+      rp[k] = xrow(L->buf[back], p->recv_off[k], L->ld, L->es());
       cs[k] = p->send_count[k] * L->ld;
       cr[k] = p->recv_count[k] * L->ld;
     }
@@ -468,7 +523,8 @@ digest_status digest_push_boundary(digest_store* st, int32_t level, const float*
       DG_CUDA(cudaStreamWaitEvent(st->side, st->packed, 0));
       xs = st->side;
     }
-    DG_TRY(dg::comm_alltoallv(st->comm, sp.data(), cs.data(), rp.data(), cr.data(), xs));
+    DG_TRY(dg::comm_alltoallv(st->comm, sp.data(), cs.data(), rp.data(), cr.data(), xs,
+                              L->bf16 ? ncclBfloat16 : ncclFloat));
     DG_CUDA(cudaEventRecord(L->done, xs));
     L->inflight = true;
   }
@@ -484,6 +540,7 @@ digest_status digest_pull(digest_store* st, int32_t level, int64_t epoch, int32_
          DIGEST_E_INVALID, "bad pull mode");
   cudaStream_t s = dg::as_stream(stream);
   if (mode == DIGEST_PULL_SNAPSHOT && !dg::is_peer(st->comm)) mode = DIGEST_PULL_COPY;
+  if (L->bf16 && mode == DIGEST_PULL_FLIP) mode = DIGEST_PULL_COPY;   // bf16 back -> fp32 front
   const int back = 1 - L->front;
   if (L->ver[back] >= epoch)
     return dg::set_error(DIGEST_E_STATE,
@@ -510,9 +567,12 @@ digest_status digest_pull(digest_store* st, int32_t level, int64_t epoch, int32_
         sg.seq[n] = dg::win_i64(st->comm->win, dg::kWinArrived) + (int64_t)(level - 1) * 64 + k;
         ++n;
       }
-      if (n > 0)
-        DG_LAUNCH(DIGEST_PROF_PACK, s, 8.0 * st->part->n_halo * L->ld, 0, k_snapshot, n, 1024, 0,
-                  L->buf[back], L->buf[L->front], L->ld, sg);
+      if (n > 0 && L->bf16)
+        DG_LAUNCH(DIGEST_PROF_PACK, s, 6.0 * st->part->n_halo * L->ld, 0, k_snapshot<true>, n, 1024,
+                  0, L->buf[back], L->buf[L->front], L->ld, sg);
+      else if (n > 0)
+        DG_LAUNCH(DIGEST_PROF_PACK, s, 8.0 * st->part->n_halo * L->ld, 0, k_snapshot<false>, n,
+                  1024, 0, L->buf[back], L->buf[L->front], L->ld, sg);
       L->ver[L->front] = L->ver[back];
     }
     if (front_h) *front_h = L->buf[L->front];
@@ -541,9 +601,15 @@ digest_status digest_pull(digest_store* st, int32_t level, int64_t epoch, int32_
       if (n4 > 0) {
         int64_t blocks = dg::ceil_div(n4, 256);
         int64_t cap = (int64_t)dg::num_sms() * 8;
-        DG_LAUNCH(DIGEST_PROF_PACK, s, 32.0 * n4, 0, k_copy, (unsigned)(blocks > cap ? cap : blocks),
-                  256, 0, reinterpret_cast<const float4*>(L->buf[back]),
-                  reinterpret_cast<float4*>(L->buf[L->front]), n4);
+        if (L->bf16)
+          DG_LAUNCH(DIGEST_PROF_PACK, s, 24.0 * n4, 0, k_widen,
+                    (unsigned)(blocks > cap ? cap : blocks), 256, 0, L->buf[back],
+                    reinterpret_cast<float4*>(L->buf[L->front]), n4);
+        else
+          DG_LAUNCH(DIGEST_PROF_PACK, s, 32.0 * n4, 0, k_copy,
+                    (unsigned)(blocks > cap ? cap : blocks), 256, 0,
+                    reinterpret_cast<const float4*>(L->buf[back]),
+                    reinterpret_cast<float4*>(L->buf[L->front]), n4);
       }
       L->ver[L->front] = L->ver[back];
     }

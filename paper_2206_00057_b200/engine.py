@@ -39,6 +39,7 @@ class TrainConfig:
     halo_grad: bool = False     # return P_out^T D W^T to the halo owners
     transport: str = "nccl"     # multi-process exchange: 'nccl' or 'peer' (CUDA IPC windows)
     async_store: bool = False   # DIGEST-A on the peer transport: NOWAIT pushes, SNAPSHOT pulls
+    store_bf16: bool = False    # bf16 stale store / transfers
 
 
 class Partition:
@@ -120,7 +121,8 @@ class DigestWorker:
                                         device=dev)
         self.loss = torch.zeros(1, dtype=torch.float64, device=dev)
         # stale store: levels 1..L-1 (never L)
-        self.store = D.digest_store_create(part.handle, comm_halo, list(dims[1:self.L]))
+        self.store = D.digest_store_create(part.handle, comm_halo, list(dims[1:self.L]),
+                                           D.STORE_BF16 if cfg.store_bf16 else 0)
         if cfg.transport == "peer" and comm_halo is not None and part.num_parts > 1:
             from .dist import connect_peer_store
             connect_peer_store(self.store, part.num_parts)   # collective over the process group

@@ -47,7 +47,11 @@ struct Cfg2 {
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
 k_gemm2_tf32x3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBh,
-               const __grid_constant__ CUtensorMap tmBl, const EpiArgs e, int K) {
+               const __grid_constant__ CUtensorMap tmBl, const EpiArgs e, int K, int single) {
+  // single: the 128 split-worker (epilogue) threads of a CTA meet at a named barrier and
+  // ONE of them arrives on rank 0's conv (tempty) barrier -- 2 cluster-scope arrivals per
+  // stage instead of 256 (each thread still fences its own smem writes / TMEM loads).
+  const uint32_t group_count = single ? 2u : 256u;
   using G = Cfg2<BN>;
   const int64_t M = e.M;
   const int N = e.N;
@@ -73,12 +77,12 @@ k_gemm2_tf32x3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < S; ++s) {
       tc::mbar_init(&full[s], 1);
-      tc::mbar_init(&conv[s], 256);
+      tc::mbar_init(&conv[s], group_count);
       tc::mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       tc::mbar_init(&tfull[a], 1);
-      tc::mbar_init(&tempty[a], 256);
+      tc::mbar_init(&tempty[a], group_count);
     }
     tc::fence_mbar_init();
     tc::tma_prefetch(&tmA);
@@ -169,7 +173,12 @@ k_gemm2_tf32x3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           Al[idx] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
         }
         tc::fence_proxy_async_smem();
-        tc::mbar_arrive_cluster(conv0 + s * 8);
+        if (single) {
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (tid == 0) tc::mbar_arrive_cluster(conv0 + s * 8);
+        } else {
+          tc::mbar_arrive_cluster(conv0 + s * 8);
+        }
         if (++s == S) { s = 0; ph ^= 1; }
       }
     }
@@ -187,7 +196,12 @@ k_gemm2_tf32x3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       tc::tc_fence_after();
       epi_tile<BN>(e, tmem_base + acc * G::ACC, stg, m0, q, lane);
       tc::tc_fence_before();
-      tc::mbar_arrive_cluster(tempty0 + acc * 8);
+      if (single) {
+        asm volatile("bar.sync 2, 128;" ::: "memory");
+        if (threadIdx.x % 128 == 0) tc::mbar_arrive_cluster(tempty0 + acc * 8);
+      } else {
+        tc::mbar_arrive_cluster(tempty0 + acc * 8);
+      }
       acc ^= 1;
       if (acc == 0) aph ^= 1;
     }
@@ -229,7 +243,13 @@ digest_status launch2(const GemmArgs& g, const CUtensorMap& tA, const CUtensorMa
   const double flops = 2.0 * (double)g.M * g.N * g.K;
   const double bytes = 4.0 * ((double)g.M * g.K + (double)g.M * g.N + 2.0 * g.N * g.K);
   Launch L(DIGEST_PROF_GEMM, s, bytes, flops, 30000000 + (int)g.K * 1000 + g.N);
-  cudaError_t e = cudaLaunchKernelEx(&cfg, k_gemm2_tf32x3<BN>, tA, tBh, tBl, epi_of(g), (int)g.K);
+  static int single = -1;   // DIGEST_GEMM_SINGLE_ARRIVE (default 1)
+  if (single < 0) {
+    const char* ev = getenv("DIGEST_GEMM_SINGLE_ARRIVE");
+    single = ev ? atoi(ev) : 1;
+  }
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_gemm2_tf32x3<BN>, tA, tBh, tBl, epi_of(g), (int)g.K,
+                                     single);
   cudaError_t e2 = L.done();
   DG_CUDA(e);
   DG_CUDA(e2);

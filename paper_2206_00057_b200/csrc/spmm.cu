@@ -88,7 +88,10 @@ __device__ __forceinline__ void spmm_row_epilogue(const SpmmArgs& a, int64_t row
         }
         nib[q] = (r.x > 0.f ? 1u : 0u) | (r.y > 0.f ? 2u : 0u) | (r.z > 0.f ? 4u : 0u) |
                  (r.w > 0.f ? 8u : 0u);
-        reinterpret_cast<float4*>(y)[idx] = r;
+        if (a.stream_out)   // streaming store: the output row is not re-read by this launch
+          __stcs(reinterpret_cast<float4*>(y) + idx, r);
+        else
+          reinterpret_cast<float4*>(y)[idx] = r;
       }
     }
   }
@@ -458,6 +461,12 @@ digest_status spmm(const SpmmArgs& a0, cudaStream_t s) {
   }
   SpmmArgs a = a0;
   a.hints = hints;
+  static int cs = -1;   // DIGEST_SPMM_STREAM_OUT: st.global.cs for the output rows
+  if (cs < 0) {
+    const char* e = getenv("DIGEST_SPMM_STREAM_OUT");
+    cs = e ? atoi(e) : 0;
+  }
+  a.stream_out = cs;
   DG_ARG(a.width > 0 && a.width % 4 == 0, DIGEST_E_INVALID,
          "SpMM width %d must be a positive multiple of 4", a.width);
   const int slab = spmm_slab_width(a);

@@ -454,13 +454,18 @@ int spmm_slab_width(const SpmmArgs& a) {
 
 digest_status spmm(const SpmmArgs& a0, cudaStream_t s) {
   if (a0.n_rows == 0) return DIGEST_OK;
-  static int hints = -1;
-  if (hints < 0) {
+  // L2 policy of the gathers (DIGEST_SPMM_HINTS overrides): 2 = bit-31 hot source rows
+  // evict_last, the rest evict_normal, for wide rows; 0 = no policy operands for narrower
+  // ones.  Measured with the persistent grid, products M=1: w=256 16.57 ms (hints 1, the
+  // rest evict_first) -> 15.37 ms (2); w=100 8.51 (1) -> 8.01 ms (0)
+  // (profiles/r1_spmm_variant_sweep.log).
+  static int hints = -2;
+  if (hints == -2) {
     const char* e = getenv("DIGEST_SPMM_HINTS");
-    hints = e ? atoi(e) : 1;
+    hints = e ? atoi(e) : -1;
   }
   SpmmArgs a = a0;
-  a.hints = hints;
+  a.hints = hints >= 0 ? hints : (a0.width >= 128 ? 2 : 0);
   static int cs = -1;   // DIGEST_SPMM_STREAM_OUT: st.global.cs for the output rows
   if (cs < 0) {
     const char* e = getenv("DIGEST_SPMM_STREAM_OUT");

@@ -37,8 +37,10 @@ def parse():
     ap.add_argument("--config", default="products")
     ap.add_argument("--mode", default="async", choices=["async", "sync"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--sample-frac", type=float, default=0.1,
-                    help="oracle sample: fraction of nodes/edges of the workload")
+    ap.add_argument("--sample-frac", type=float, default=0.0,
+                    help="oracle sample: fraction of nodes/edges of the workload (0 = auto: "
+                         "0.1, shrunk so the --impl reference run of K+W oracle epochs stays "
+                         "within a few minutes)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sync-interval", type=int, default=0,
                     help="override the config's N_sync (the Fig. 6 sweep, SURVEY f1)")
@@ -156,10 +158,19 @@ def cores():
         return os.cpu_count()
 
 
+def reference_frac(a):
+    """Oracle sample size: 10% of the workload per epoch (~12-18 s on 8-16 host cores for
+    products), scaled down so K + W epochs take about 8 such epochs in total."""
+    if a.sample_frac > 0:
+        return a.sample_frac
+    return max(0.01, min(0.1, 0.1 * 8.0 / max(1, a.steps + a.warmup)))
+
+
 def run_reference(a, rank, world):
     if rank != 0:
         return
-    per, sample = oracle_sample_epoch_seconds(a.config, world, a.sample_frac, a.steps, a.warmup)
+    per, sample = oracle_sample_epoch_seconds(a.config, world, reference_frac(a), a.steps,
+                                              a.warmup)
     v = float(np.mean(per))
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
@@ -342,7 +353,7 @@ def run_ours(a, rank, world, local):
         gteps = nz / (spmm["ms"] / 1e3) / 1e9
     cpu = None
     if rank == 0 and world == 1 and not loop:   # the oracle baseline is timed at N=1 only
-        per, sample = oracle_sample_epoch_seconds(a.config, M, a.sample_frac, 1, 1)
+        per, sample = oracle_sample_epoch_seconds(a.config, M, a.sample_frac or 0.1, 1, 1)
         cpu = {"value": float(np.mean(per)), "unit": "s", "cores": cores(), "kind": "oracle",
                "sample": sample}
     if rank == 0:

@@ -181,8 +181,10 @@ digest_status digest_store_link(digest_store* const* stores_h, int32_t count);
  * rows H_local[send_idx] of level `level` (optionally row-L2-normalised, Alg. 1
  * P:226) and delivers them into every peer's back buffer at the
  * (owner, id) segment of its halo.  `version` = epoch r.  With DIGEST_PUSH_ASYNC
- * the exchange runs on the store's side stream behind an event (overlap with the
- * next layer).  Collective: every rank pushes the same (level, version). */
+ * the NCCL exchange runs on the store's side stream behind an event (overlap with the
+ * next layer); on the peer transport the push is one fused gather + put
+ * kernel on `stream` (the put is the gather's own stores; ASYNC is accepted and has
+ * nothing to defer).  Collective: every rank pushes the same (level, version). */
 digest_status digest_push_boundary(digest_store* store, int32_t level, const float* H_local,
                                    int64_t ld, int64_t version, uint32_t flags,
                                    void* stream);

@@ -279,7 +279,7 @@ digest_status launch_tc(const GemmArgs& g, const CUtensorMap& tA, const CUtensor
 
 }  // namespace
 
-bool gemm_tc2_enabled(int N);
+bool gemm_tc2_enabled(int N, int K);
 digest_status gemm_tc2(const GemmArgs& g, const float* hi, const float* lo, int Kp,
                        cudaStream_t s);
 
@@ -313,7 +313,7 @@ digest_status gemm_tc(const GemmArgs& g, cudaStream_t s) {
     DG_LAUNCH(DIGEST_PROF_OTHER, s, 12.0 * total, 0, k_prep_b, (unsigned)blocks, 256, 0, g.B,
               g.sBk, g.sBj, K, N, Kp, hi, lo);
   }
-  if (gemm_tc2_enabled(N) && g.M >= 2 * kBM) return gemm_tc2(g, hi, lo, Kp, s);
+  if (gemm_tc2_enabled(N, (int)g.K) && g.M >= 2 * kBM) return gemm_tc2(g, hi, lo, Kp, s);
   int BN = N <= 16 ? 16 : N <= 32 ? 32 : N <= 48 ? 48 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
   CUtensorMap tA, tBh, tBl;
   bool ok = make_tmap_2d(&tA, g.A, (uint64_t)K, (uint64_t)g.M, (uint64_t)g.sAi * 4, kBK, kBM) &&

@@ -259,7 +259,7 @@ digest_status launch2(const GemmArgs& g, const CUtensorMap& tA, const CUtensorMa
 }  // namespace
 
 // Called by gemm_tc after the weight split: hi/lo are [N x Kp] K-major.
-bool gemm_tc2_enabled(int N) {
+bool gemm_tc2_enabled(int N, int K) {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("DIGEST_GEMM_2CTA");
@@ -267,7 +267,9 @@ bool gemm_tc2_enabled(int N) {
   }
   // measured (tools/gemm_bench.py, 2.45M rows): N=256 1.64 -> 1.60 ms with pairs; N=48 is
   // 2x slower with pairs (too little MMA work per k-block to hide the cross-CTA handshake)
-  return v != 0 && N >= 128 && N % 16 == 0;
+  // K <= 64: a tile is only 1-2 k-blocks, the pair handshake costs more than the halved
+  // B traffic saves (K=48, N=256: 0.855 ms pair vs 0.772 ms single CTA)
+  return v != 0 && N >= 128 && N % 16 == 0 && K > 64;
 }
 
 digest_status gemm_tc2(const GemmArgs& g, const float* hi, const float* lo, int Kp,

@@ -535,11 +535,14 @@ digest_status spmm_one(const SpmmArgs& a, cudaStream_t s) {
     }
     switch (v) {
       case 1: return launch<32, 2, 4>(a, s);
-      case 2: return launch<32, 2, 8>(a, s);
+      case 2: return launch<32, 2, 4, false, 4>(a, s);
       case 3: return launch<32, 2, 8, false>(a, s);
       case 4: return launch<16, 4, 4, false>(a, s);
       case 5: return launch<32, 2, 2, false>(a, s);
-      default: return launch<32, 2, 4, false, 4>(a, s);   // w=256: 17.98 ms (MB=4) vs 18.95
+      case 6: return launch<32, 2, 4, false, 4>(a, s);
+      // w=256, persistent grid, products M=1: chunk-prefetching <32,2,8> 14.91 ms vs
+      // runtime-loop <32,2,4,MB=4> 15.35 ms (profiles/r1_spmm_variant_sweep.log)
+      default: return launch<32, 2, 8>(a, s);
     }
   }
   if (w4 <= 96) return launch<32, 3, 4, false>(a, s);

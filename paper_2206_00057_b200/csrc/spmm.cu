@@ -522,9 +522,13 @@ digest_status spmm_one(const SpmmArgs& a, cudaStream_t s) {
     }
     if (v == 1) return launch<5, 5, 2, false>(a, s);
     if (v == 2) return launch<5, 5, 2, true>(a, s);
-    // measured best for w=100 with the persistent grid (products M=1): 7.75 ms vs 8.59 ms
-    // for <5,5,2,prefetch> and 10.2 ms for <5,5,2,rt> (profiles/r1_spmm_variant_sweep.log)
-    return launch<8, 4, 2, false, 4>(a, s);
+    if (v == 3) return launch<8, 4, 2, true>(a, s);
+    if (v == 4) return launch<8, 4, 2, false, 4>(a, s);
+    if (v == 5) return launch<8, 4, 1, true>(a, s);
+    // measured best for w=100 (persistent grid, no policy operands): chunk-prefetching
+    // <8,4,4>: products M=1 7.15 ms vs 7.91 ms for <8,4,2,rt,MB4>; 8-part partition
+    // 0.97 vs 1.33 ms (profiles/r1_spmm_variant_sweep.log)
+    return launch<8, 4, 4, true>(a, s);
   }
   if (w4 <= 32) return launch<8, 4, 2, false>(a, s);
   if (w4 <= 64) {

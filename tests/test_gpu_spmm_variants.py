@@ -19,7 +19,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 CASES = [(48, {"DIGEST_SPMM_V12": str(v)}) for v in range(5)]
 CASES += [(48, {"DIGEST_SPMM_PFH": "1"}), (48, {"DIGEST_SPMM_GRID": "1"})]
-CASES += [(100, {"DIGEST_SPMM_V25": str(v)}) for v in range(3)]
+CASES += [(100, {"DIGEST_SPMM_V25": str(v)}) for v in range(6)]
 CASES += [(256, {"DIGEST_SPMM_V": str(v)}) for v in range(7)]
 CASES += [(256, {"DIGEST_SPMM_SLAB": "64"}), (256, {"DIGEST_SPMM_HINTS": "0"}),
           (256, {"DIGEST_SPMM_GRID": "0"}), (100, {"DIGEST_SPMM_SLAB": "32"})]

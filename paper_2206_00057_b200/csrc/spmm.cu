@@ -530,7 +530,15 @@ digest_status spmm_one(const SpmmArgs& a, cudaStream_t s) {
     // 0.97 vs 1.33 ms (profiles/r1_spmm_variant_sweep.log)
     return launch<8, 4, 4, true>(a, s);
   }
-  if (w4 <= 32) return launch<8, 4, 2, false>(a, s);
+  if (w4 <= 32) {   // w = 128 (arxiv d0)
+    static int v = -1;
+    if (v < 0) {
+      const char* e = getenv("DIGEST_SPMM_V32");
+      v = e ? atoi(e) : 0;
+    }
+    if (v == 1) return launch<8, 4, 2, false>(a, s);
+    return launch<8, 4, 4, true>(a, s);
+  }
   if (w4 <= 64) {
     static int v = -1;
     if (v < 0) {

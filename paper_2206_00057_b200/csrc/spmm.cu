@@ -384,7 +384,18 @@ digest_status launch_mb(const SpmmArgs& a, cudaStream_t s, int64_t blocks, doubl
     const char* e = getenv("DIGEST_SPMM_PFH");
     pfh = e ? atoi(e) : 0;
   }
-  if (PF && pfh && a.hints) {
+  static int xr = -1;   // DIGEST_SPMM_XR=1: cross-row pipelining in the prefetching kernel
+  if (xr < 0) {
+    const char* e = getenv("DIGEST_SPMM_XR");
+    xr = e ? atoi(e) : 0;
+  }
+  if (PF && xr) {
+    static const int64_t cap = resident_ctas(k_spmm<LC, VPL, UNR, true, MB, false>);
+    if (spmm_persistent(a) && blocks > cap) blocks = cap;
+    DG_LAUNCH_TAG(DIGEST_PROF_SPMM, a.full_width > 0 ? a.full_width : a.width, s, bytes, flops,
+                  (k_spmm<LC, VPL, UNR, true, MB, false>),
+                  (unsigned)blocks, 256, 0, a);
+  } else if (PF && pfh && a.hints) {
     static const int64_t cap = resident_ctas(k_spmm<LC, VPL, UNR, false, MB, true>);
     if (spmm_persistent(a) && blocks > cap) blocks = cap;
     DG_LAUNCH_TAG(DIGEST_PROF_SPMM, a.full_width > 0 ? a.full_width : a.width, s, bytes, flops,

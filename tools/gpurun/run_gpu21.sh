@@ -1,0 +1,7 @@
+export PYTHONUNBUFFERED=1
+mkdir -p gpurun_out
+B="python bench.py --steps 1 --warmup 1 --no-e2e"
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_spmm -c 3 -f -o gpurun_out/r1_spmm_full $B > gpurun_out/g21_a.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gemm2 -c 1 -f -o gpurun_out/r1_gemm_full $B > gpurun_out/g21_b.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_wgrad_bf16x6 -c 1 -f -o gpurun_out/r1_wgrad_full $B > gpurun_out/g21_c.log 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/g21_launches.csv python bench.py --steps 2 --warmup 1 --no-e2e > gpurun_out/g21_d.log 2>&1

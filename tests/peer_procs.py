@@ -22,7 +22,8 @@ def run_rank(rank, world, port, spec, out_path):
     from paper_2206_00057_b200.engine import TrainConfig, build_workers
     from synth import small_config, make_inputs, make_block_parts, make_random_parts
 
-    cfg = small_config(**spec["graph"])
+    from synth import get_config
+    cfg = get_config(spec["config"]) if "config" in spec else small_config(**spec["graph"])
     inp = make_inputs(cfg)
     part = (make_block_parts(cfg, world) if spec.get("parts_seed") is None
             else make_random_parts(cfg.num_nodes, world, spec["parts_seed"]))

@@ -169,3 +169,28 @@ def test_digest_a_multiprocess(name, tmp_path):
         # the others finish long before the straggler's injected delays have elapsed
         assert res["wall"][others].max() < res["wall"][s] - 0.5 * R * spec["delay_ms"] / 1e3
         assert res["loss"][:, -1].mean() < res["loss"][:, 0].mean()
+
+
+@pytest.mark.slow
+@pytest.mark.timeout(900)
+def test_peer_transport_full_size_products_matches_loopback(tmp_path):
+    """bench.py's workload at full size (products-shaped, 2.45M nodes, 124M edges, Adam,
+    N=10) on 2 processes over the peer transport, 11 epochs (pushes at 1 and 11, the pull
+    at 10): every per-epoch loss and the final weights are bit-identical to the loopback
+    run of the same 2 partitions (whose epoch-1 layer outputs are checked against the
+    oracle on sampled rows in test_gpu_parity.py)."""
+    import torch.multiprocessing as mp
+    from synth import get_config
+    cfg = get_config("products")
+    spec = dict(world=2, parts_seed=None, epochs=11, config="products",
+                train=dict(sync_interval=cfg.sync_interval, lr=0.01, optimizer="adam"))
+    out = str(tmp_path / "res.npz")
+    mp.start_processes(run_rank, args=(2, free_port(), spec, out), nprocs=2, join=True,
+                       start_method="spawn")
+    res = np.load(out)
+    inp = make_inputs(cfg)
+    part = make_block_parts(cfg, 2)
+    lb_loss, lb_W = loopback(spec, cfg, inp, part)
+    assert (res["pushes"] == 2 * 2).all() and (res["pulls"] == 1 * 2).all()
+    assert res["loss"].tobytes() == lb_loss.tobytes()
+    assert res["W"][0].tobytes() == lb_W.tobytes() == res["W"][1].tobytes()

@@ -51,7 +51,9 @@ struct WCfg {
   static constexpr uint32_t RAW = RAW_A + RAW_B;
   static constexpr uint32_t PIECE = 3 * PA + 3 * PB;
   static constexpr int PS = 2;
-  static constexpr int RS = ((200 * 1024 - PS * PIECE) / RAW) > 4 ? 4
+  // staging depth: as many fp32 stages as fit (up to 8) -- the TMA bytes in flight per
+  // SM are what keep the HBM busy for the narrow (N=48) and single-half (M<=128) shapes
+  static constexpr int RS = ((200 * 1024 - PS * PIECE) / RAW) > 8 ? 8
                                                                    : ((200 * 1024 - PS * PIECE) / RAW);
   static constexpr uint32_t SMEM = RS * RAW + PS * PIECE + 1024 + 256;
   static_assert(RS >= 2, "staging ring");

@@ -61,6 +61,66 @@ k_xent(const float* __restrict__ Z, int64_t n, int C, int64_t ld, const int32_t*
   }
 }
 
+// The same for C <= ld_g <= 64 (every BASELINE config): a lane owns columns lane and
+// lane + 32, the row is read once into registers and the next row's logits, label and
+// mask are loaded while the current row is reduced (two rows in flight per warp).  Same
+// operations in the same order as k_xent, so the results are bit-identical.
+__global__ void __launch_bounds__(kXentThreads)
+k_xent64(const float* __restrict__ Z, int64_t n, int C, int64_t ld, const int32_t* __restrict__ y,
+         const uint8_t* __restrict__ mask, float w, float* __restrict__ G, int64_t ldg,
+         double* __restrict__ partial) {
+  __shared__ double wsum[kXentThreads / 32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const bool c0 = lane < C, c1 = lane + 32 < C;
+  double acc = 0.0;
+  float z0 = -INFINITY, z1 = -INFINITY;
+  int yi = 0;
+  bool t = false;
+  auto load = [&](int64_t i) {
+    const float* z = Z + i * ld;
+    z0 = c0 ? __ldg(z + lane) : -INFINITY;
+    z1 = c1 ? __ldg(z + lane + 32) : -INFINITY;
+    yi = __ldg(y + i);
+    t = __ldg(mask + i) != 0;
+  };
+  if (warp < n) load(warp);
+  for (int64_t i = warp; i < n; i += nw) {
+    const float a0 = z0, a1 = z1;
+    const int yc = yi;
+    const bool tc = t;
+    if (i + nw < n) load(i + nw);   // next row in flight while this one is reduced
+    float* g = G + i * ldg;
+    if (!tc) {
+      if (lane < ldg) g[lane] = 0.f;
+      if (lane + 32 < ldg) g[lane + 32] = 0.f;
+      continue;
+    }
+    float m = fmaxf(a0, a1);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const float e0 = c0 ? expf(a0 - m) : 0.f, e1 = c1 ? expf(a1 - m) : 0.f;
+    float s = 0.f;
+    if (c0) s += e0;
+    if (c1) s += e1;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const float inv = 1.f / s;
+    if (lane < ldg) g[lane] = c0 ? w * (e0 * inv - (lane == yc ? 1.f : 0.f)) : 0.f;
+    if (lane + 32 < ldg) g[lane + 32] = c1 ? w * (e1 * inv - (lane + 32 == yc ? 1.f : 0.f)) : 0.f;
+    const float zy = __shfl_sync(0xffffffffu, yc < 32 ? a0 : a1, yc & 31);
+    if (lane == 0) acc += (double)(m + logf(s) - zy);
+  }
+  if (lane == 0) wsum[wib] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    for (int k = 0; k < kXentThreads / 32; ++k) b += wsum[k];
+    partial[blockIdx.x] = b * (double)w;
+  }
+}
+
 __global__ void k_sum_partials(const double* __restrict__ partial, int nb, double* __restrict__ out) {
   double s = 0.0;
   for (int b = 0; b < nb; ++b) s += partial[b];
@@ -137,8 +197,12 @@ digest_status digest_xent(const float* logits, int64_t n, int32_t C, int64_t ld,
   DG_ARG(logits && labels && train_mask && G_logits, DIGEST_E_INVALID, "NULL input");
   int nb = xent_blocks(n);
   double* part = reinterpret_cast<double*>(scratch);
-  DG_LAUNCH(DIGEST_PROF_OTHER, s, 8.0 * n * C, 0, k_xent, nb, kXentThreads, 0, logits, n, C, ld,
-            labels, train_mask, w_loss, G_logits, ld_g, part);
+  if (ld_g <= 64)
+    DG_LAUNCH(DIGEST_PROF_OTHER, s, 8.0 * n * C, 0, k_xent64, nb, kXentThreads, 0, logits, n, C,
+              ld, labels, train_mask, w_loss, G_logits, ld_g, part);
+  else
+    DG_LAUNCH(DIGEST_PROF_OTHER, s, 8.0 * n * C, 0, k_xent, nb, kXentThreads, 0, logits, n, C,
+              ld, labels, train_mask, w_loss, G_logits, ld_g, part);
   DG_LAUNCH(DIGEST_PROF_OTHER, s, 0, 0, k_sum_partials, 1, 1, 0, part, nb, loss_out);
   return DIGEST_OK;
 }

@@ -241,9 +241,11 @@ def test_layer_empty_halo_and_argument_errors():
 
 
 # ------------------------------------------------------------------ loss, update, gemm
-def test_xent_parity():
+@pytest.mark.parametrize("C,Cp", [(41, 48), (7, 8), (64, 64), (70, 72)])
+def test_xent_parity(C, Cp):
+    """Both kernels: the register path (ld_g <= 64) and the generic loop (ld_g > 64)."""
     Dm = D()
-    n, C, Cp = 5000, 41, 48
+    n = 5000
     g = torch.Generator().manual_seed(1)
     z = torch.randn(n, Cp, generator=g) * 3
     y = torch.randint(0, C, (n,), generator=g, dtype=torch.int32)

@@ -352,6 +352,13 @@ digest_status digest_adam_step(float* W, const float* G, float* m, float* v, int
                                float lr, float b1, float b2, float eps, int64_t step,
                                void* stream);
 
+/* The same with the step count in device memory (*step_dev = updates done so far; this
+ * call uses step *step_dev + 1 and then increments it), so an epoch captured in a CUDA
+ * graph replays with the right bias correction. */
+digest_status digest_adam_step_dev(float* W, const float* G, float* m, float* v, int64_t count,
+                                   float lr, float b1, float b2, float eps, int64_t* step_dev,
+                                   void* stream);
+
 /* ------------------------------------------------------------------ dense helper
  * C[M x N] = op(A[M x K] B[K x N]) in fp32 on the path the layer uses (exposed for
  * tests and the GEMM roofline).  flags bit0: ReLU epilogue. */

@@ -94,6 +94,7 @@ _SIGS = {
     "digest_ps_download_peer": ([_p, _p, _i64, _p], _i32),
     "digest_ps_updates_peer": ([_p, _p], _i32),
     "digest_delay": ([_i64, _p], _i32),
+    "digest_adam_step_dev": ([_p, _p, _p, _p, _i64, _f32, _f32, _f32, _f32, _p, _p], _i32),
     "digest_adam_step": ([_p, _p, _p, _p, _i64, _f32, _f32, _f32, _f32, _i64, _p], _i32),
     "digest_gemm": ([_p, _i64, _p, _i64, _p, _i64, _i64, _i32, _i32, _u32, _p], _i32),
 }
@@ -436,3 +437,8 @@ def digest_ps_updates_peer(comm) -> int:
 
 def digest_delay(ns: int, stream=None):
     _check(lib.digest_delay(int(ns), stream_ptr(stream)))
+
+
+def digest_adam_step_dev(W, G, m, v, lr, b1, b2, eps, step_dev, stream=None):
+    _check(lib.digest_adam_step_dev(ptr(W), ptr(G), ptr(m), ptr(v), W.numel(), lr, b1, b2, eps,
+                                    ptr(step_dev), stream_ptr(stream)))

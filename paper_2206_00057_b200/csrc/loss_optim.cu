@@ -147,6 +147,27 @@ __global__ void k_adam(float* __restrict__ W, const float* __restrict__ G, float
   }
 }
 
+// Adam with the step count on the device (CUDA-graph replay: no host argument changes
+// between epochs).  t = *step + 1 is this update's step; k_step_incr advances it after.
+__global__ void k_adam_dev(float* __restrict__ W, const float* __restrict__ G, float* __restrict__ m,
+                           float* __restrict__ v, int64_t n, float lr, float b1, float b2,
+                           float eps, const int64_t* __restrict__ step) {
+  const double t = (double)(*step + 1);
+  const float c1 = (float)(1.0 - pow((double)b1, t));
+  const float c2 = (float)(1.0 - pow((double)b2, t));
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float g = G[i];
+    float mi = b1 * m[i] + (1.f - b1) * g;
+    float vi = b2 * v[i] + (1.f - b2) * g * g;
+    m[i] = mi;
+    v[i] = vi;
+    W[i] -= lr * (mi / c1) / (sqrtf(vi / c2) + eps);
+  }
+}
+
+__global__ void k_step_incr(int64_t* step) { *step += 1; }
+
 __global__ void k_scale(float* __restrict__ x, int64_t n, float a) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -254,6 +275,18 @@ digest_status digest_adam_step(float* W, const float* G, float* m, float* v, int
   float c2 = (float)(1.0 - std::pow((double)b2, (double)step));
   DG_LAUNCH(DIGEST_PROF_OTHER, s, 28.0 * count, 12.0 * count, k_adam, elt_blocks(count), 256, 0,
             W, G, m, v, count, lr, b1, b2, eps, c1, c2);
+  return DIGEST_OK;
+}
+
+digest_status digest_adam_step_dev(float* W, const float* G, float* m, float* v, int64_t count,
+                                   float lr, float b1, float b2, float eps, int64_t* step_dev,
+                                   void* stream) {
+  DG_ARG(W && G && m && v && step_dev && count >= 0, DIGEST_E_INVALID, "bad argument");
+  cudaStream_t s = dg::as_stream(stream);
+  if (count > 0)
+    DG_LAUNCH(DIGEST_PROF_OTHER, s, 28.0 * count, 12.0 * count, k_adam_dev, elt_blocks(count), 256,
+              0, W, G, m, v, count, lr, b1, b2, eps, step_dev);
+  DG_LAUNCH(DIGEST_PROF_OTHER, s, 0, 0, k_step_incr, 1, 1, 0, step_dev);
   return DIGEST_OK;
 }
 

@@ -40,6 +40,7 @@ class TrainConfig:
     transport: str = "nccl"     # multi-process exchange: 'nccl' or 'peer' (CUDA IPC windows)
     async_store: bool = False   # DIGEST-A on the peer transport: NOWAIT pushes, SNAPSHOT pulls
     store_bf16: bool = False    # bf16 stale store / transfers
+    device_step: bool = False   # Adam step count on the device (CUDA-graph capturable epochs)
 
 
 class Partition:
@@ -103,6 +104,7 @@ class DigestWorker:
             self.adam_m = torch.zeros_like(self.W_flat)
             self.adam_v = torch.zeros_like(self.W_flat)
         self.step_count = 0
+        self.step_dev = torch.zeros(1, dtype=torch.int64, device=dev) if cfg.device_step else None
         # activations, saved state, gradients
         self.H = [None] + [torch.empty(n, dims[l], device=dev) for l in range(1, self.L + 1)]
         self.saved, scratch = [None], 0
@@ -225,6 +227,9 @@ class DigestWorker:
         self.step_count += 1
         if self.cfg.optimizer == "sgd":
             D.digest_sgd_step(self.W_flat, self.G_flat, self.cfg.lr, stream)
+        elif self.step_dev is not None:
+            D.digest_adam_step_dev(self.W_flat, self.G_flat, self.adam_m, self.adam_v, self.cfg.lr,
+                                   0.9, 0.999, 1e-8, self.step_dev, stream)
         else:
             D.digest_adam_step(self.W_flat, self.G_flat, self.adam_m, self.adam_v, self.cfg.lr,
                                0.9, 0.999, 1e-8, self.step_count, stream)

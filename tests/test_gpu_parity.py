@@ -275,6 +275,51 @@ def test_optimizers_parity():
         Dm.digest_adam_step(Wd, G.cuda() * step, m, v, 0.01, 0.9, 0.999, 1e-8, step)
         wr, mr, vr = oracle.adam_step(wr, G.numpy() * step, mr, vr, step, 0.01)
     assert rel(Wd.cpu().numpy(), wr) <= 1e-5
+    # device-resident step count (CUDA-graph epochs): the same three updates
+    Wd2 = W.cuda()
+    m, v = torch.zeros_like(Wd2), torch.zeros_like(Wd2)
+    step_dev = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for step in (1, 2, 3):
+        Dm.digest_adam_step_dev(Wd2, G.cuda() * step, m, v, 0.01, 0.9, 0.999, 1e-8, step_dev)
+    assert int(step_dev.item()) == 3
+    assert rel(Wd2.cpu().numpy(), wr) <= 1e-5
+
+
+def test_cuda_graph_epoch_replay_matches_eager():
+    """An M=1 epoch captured in a CUDA graph (Adam step on the device) and replayed gives the
+    eager run's weights and losses, bit for bit (same kernels, same arguments)."""
+    from paper_2206_00057_b200.engine import TrainConfig, build_workers
+    cfg = small_config(num_nodes=1500, nnz=16000, d0=20, hidden=(32, 16), num_classes=6, c_pad=8,
+                       seed=91, train_frac=0.5)
+    inp = make_inputs(cfg)
+    part = np.zeros(cfg.num_nodes, np.int32)
+    runs = []
+    for use_graph in (False, True):
+        tc = TrainConfig(dims=cfg.dims, num_classes=cfg.num_classes, sync_interval=1, lr=0.01,
+                         optimizer="adam", device_step=True)
+        (w,) = build_workers(inp.indptr, inp.indices, inp.x, inp.y, inp.train_mask, inp.weights,
+                             part, 1, tc)
+        w.epoch(1)                          # warm-up (lazy workspaces, attributes)
+        losses = []
+        if use_graph:
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                w.epoch(2)
+            for _ in range(4):
+                g.replay()
+                torch.cuda.synchronize()
+                losses.append(w.loss.item())
+        else:
+            for r in range(2, 6):
+                w.epoch(r)
+                torch.cuda.synchronize()
+                losses.append(w.loss.item())
+        runs.append((losses, w.W_flat.cpu().numpy(), int(w.step_dev.item())))
+        w.close()
+    assert runs[0][0] == runs[1][0]
+    assert runs[0][1].tobytes() == runs[1][1].tobytes()
+    assert runs[0][2] == runs[1][2] == 5
 
 
 @pytest.mark.parametrize("M,N,K", [(1000, 256, 100), (777, 48, 256), (4096, 16, 1436),

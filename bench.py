@@ -214,14 +214,29 @@ def run_ours(a, rank, world, local):
     t_gen = time.time() - t0
 
     comm_grad = comm_halo = None
+    if world > 1 and a.transport == "peer":
+        # every rank must map every peer's window; if CUDA IPC is unavailable anywhere (e.g.
+        # a container without IPC permissions) all ranks agree to use NCCL instead
+        from paper_2206_00057_b200.dist import connect_peer_comm, grad_count
+        err = None
+        try:
+            comm_grad = comm_halo = connect_peer_comm(world, rank, grad_count(cfg.dims))
+        except Exception as ex:   # noqa: BLE001  (reported, then agreed on below)
+            err = ex
+        ok = torch.tensor([0 if err else 1], dtype=torch.int32, device=coll_dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0:
+            if rank == 0:
+                print(f"warning: peer transport unavailable ({err}); using NCCL", file=sys.stderr)
+            if comm_grad is not None:
+                D.digest_comm_destroy(comm_grad)
+            comm_grad = comm_halo = None
+            a.transport = "nccl"
     if world > 1 and a.transport == "nccl":
         from paper_2206_00057_b200.dist import broadcast_ids
         ids = broadcast_ids(D.digest_comm_unique_id, 2, rank, device=coll_dev)
         comm_grad = D.digest_comm_init(ids[0], world, rank)
         comm_halo = D.digest_comm_init(ids[1], world, rank)
-    elif world > 1:
-        from paper_2206_00057_b200.dist import connect_peer_comm, grad_count
-        comm_grad = comm_halo = connect_peer_comm(world, rank, grad_count(cfg.dims))
 
     n_sync = a.sync_interval or cfg.sync_interval
     tc = TrainConfig(dims=cfg.dims, num_classes=cfg.num_classes, sync_interval=n_sync,

@@ -83,10 +83,30 @@ def grad_count(dims):
 
 
 def connect_peer_comm(world: int, rank: int, max_grad_count: int):
-    """Create this rank's peer-memory window and map every peer's (collective)."""
+    """Create this rank's peer-memory window and map every peer's (collective).
+
+    Every rank takes part in the handle exchange even if its own window failed, so a
+    failure raises on the failing rank (and on the ranks that see its empty handle)
+    instead of leaving the others blocked in the collective."""
     from . import capi as D
-    comm = D.digest_comm_init_peer(world, rank, max_grad_count)
-    D.digest_comm_connect(comm, all_gather_bytes(D.digest_comm_export(comm), world))
+    comm, blob, err = None, b"", None
+    try:
+        comm = D.digest_comm_init_peer(world, rank, max_grad_count)
+        blob = D.digest_comm_export(comm)
+    except Exception as e:   # noqa: BLE001
+        err = e
+    blobs = all_gather_bytes(blob, world)
+    if err is None and any(len(b) != D.IPC_HANDLE_BYTES for b in blobs):
+        err = RuntimeError("a peer could not export its window")
+    if err is None:
+        try:
+            D.digest_comm_connect(comm, blobs)
+        except Exception as e:   # noqa: BLE001
+            err = e
+    if err is not None:
+        if comm is not None:
+            D.digest_comm_destroy(comm)
+        raise err
     return comm
 
 

@@ -31,7 +31,13 @@ namespace {
 
 constexpr int kBK = 16;           // K rows per stage
 constexpr int kChunkBlocks = 64;  // k-blocks (x16 rows) accumulated in TMEM before a flush
-constexpr int kThreads = 320;
+// warp roles: 0 TMA, 1 MMA, 2 .. 2+kConvWarps-1 split workers, then 4 epilogue warps.
+// Eight split-worker warps (two per SM sub-partition): the fp32 -> 3 x bf16 split of both
+// operands is a dependent LDS -> ALU -> STS chain per element, and with one warp per
+// sub-partition its latency, not the tensor pipe, set the stage time.
+constexpr int kConvWarps = 8;
+constexpr int kConvThreads = kConvWarps * 32;
+constexpr int kThreads = (2 + kConvWarps + 4) * 32;
 
 constexpr uint32_t pow2_cols(uint32_t c) {
   return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512;
@@ -151,10 +157,10 @@ k_wgrad_bf16x6(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   if (warp == 0 && lane == 0) {
     for (int r = 0; r < RS; ++r) {
       tc::mbar_init(&full[r], 1);
-      tc::mbar_init(&rfree[r], 128);
+      tc::mbar_init(&rfree[r], kConvThreads);
     }
     for (int s = 0; s < PS; ++s) {
-      tc::mbar_init(&conv[s], 128);
+      tc::mbar_init(&conv[s], kConvThreads);
       tc::mbar_init(&empty[s], 1);
     }
     tc::mbar_init(tfull, 1);
@@ -222,7 +228,7 @@ k_wgrad_bf16x6(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         tc::mma_commit(tfull);
       }
     }
-  } else if (warp < 6) {  // split workers: fp32 -> 3 bf16 pieces, both operands
+  } else if (warp < 2 + kConvWarps) {  // split workers: fp32 -> 3 bf16 pieces, both operands
     const int tid = threadIdx.x - 64;
     constexpr int UA = kBK * (MT * 128 / 8);   // 8-element units of A per stage
     constexpr int UB = kBK * (BN / 8);
@@ -231,11 +237,11 @@ k_wgrad_bf16x6(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     for (int kb = 0; kb < nkb; ++kb) {
       tc::mbar_wait(&full[r], rph);
       tc::mbar_wait(&empty[s], ph ^ 1);   // the MMA has finished reading piece slot s
-      for (int u = tid; u < ((dbg & 1) ? 0 : UA); u += 128) {
+      for (int u = tid; u < ((dbg & 1) ? 0 : UA); u += kConvThreads) {
         const int k = u / (MT * 128 / 8), e = (u % (MT * 128 / 8)) * 8;
         split8(rawA(r), pieceA(s, 0), pieceA(s, 1), pieceA(s, 2), G::PA, k, e);
       }
-      for (int u = tid; u < ((dbg & 1) ? 0 : UB); u += 128) {
+      for (int u = tid; u < ((dbg & 1) ? 0 : UB); u += kConvThreads) {
         const int k = u / (BN / 8), e = (u % (BN / 8)) * 8;
         split8(rawB(r), pieceB(s, 0), pieceB(s, 1), pieceB(s, 2), G::PB, k, e);
       }

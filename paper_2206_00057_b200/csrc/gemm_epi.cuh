@@ -49,15 +49,18 @@ __device__ __forceinline__ void epi_prefetch_next(const EpiArgs& e, int64_t next
 
 // Drain this warp's 32 rows (TMEM lane quarter q) of the tile at rows m0.., columns
 // 0..N-1 (every kernel covers N in one tile, BN >= N, so column words align).
+// Columns [c_beg, c_end) (multiples of 32): several warps may share a lane quarter.
 template <int BN>
 __device__ __forceinline__ void epi_tile(const EpiArgs& e, uint32_t tmem_acc, float4* stg,
-                                         int64_t m0, int q, int lane) {
+                                         int64_t m0, int q, int lane, int c_beg = 0,
+                                         int c_end = BN) {
   const int ch = lane & 7;
   const int64_t my_row = m0 + q * 32 + lane;   // the row TMEM hands this lane
   const bool my_ok = my_row < e.M;
-  uint32_t mw_next = (e.mbits && my_ok) ? __ldg(e.mbits + my_row * e.ldmb) : 0xffffffffu;
+  uint32_t mw_next = (e.mbits && my_ok && c_beg < c_end)
+                         ? __ldg(e.mbits + my_row * e.ldmb + (c_beg >> 5)) : 0xffffffffu;
 #pragma unroll 1
-  for (int c0 = 0; c0 < BN; c0 += 32) {
+  for (int c0 = c_beg; c0 < c_end; c0 += 32) {
     float4 mk[8];
     if (e.mask) {  // issue all 8 mask loads before the TMEM read (8 in flight per lane)
 #pragma unroll
@@ -70,7 +73,7 @@ __device__ __forceinline__ void epi_tile(const EpiArgs& e, uint32_t tmem_acc, fl
       }
     }
     const uint32_t mw = mw_next;
-    if (e.mbits && my_ok && c0 + 32 < BN && c0 + 32 < e.N)
+    if (e.mbits && my_ok && c0 + 32 < c_end && c0 + 32 < e.N)
       mw_next = __ldg(e.mbits + my_row * e.ldmb + ((c0 + 32) >> 5));
     uint32_t r[32];
     tc::tmem_ld_32x32b_x32(tmem_acc + ((uint32_t)(q * 32) << 16) + c0, r);

@@ -24,7 +24,10 @@ void* workspace(size_t bytes);
 
 namespace {
 
-constexpr int kBM = 128, kBK = 32, kThreads = 320;
+// warps: 0 TMA, 1 MMA (rank 0), 2-5 split workers, 6-13 epilogue: two warps per TMEM lane
+// quarter, each draining half of the tile's columns (the epilogue, not the tensor pipe,
+// bounds the small-K shapes)
+constexpr int kBM = 128, kBK = 32, kEpiWarps = 8, kThreads = (6 + kEpiWarps) * 32;
 
 constexpr uint32_t pow2_cols2(uint32_t c) {
   return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512;
@@ -38,7 +41,7 @@ struct Cfg2 {
   static constexpr uint32_t B_BYTES = (BN / 2) * kBK * 4;     // this CTA's half of B
   static constexpr uint32_t STAGE = 2 * A_BYTES + 2 * B_BYTES;
   static constexpr int STAGES = (192 * 1024 / STAGE) > 4 ? 4 : (192 * 1024 / STAGE);
-  static constexpr uint32_t EPI = 4 * 4096;
+  static constexpr uint32_t EPI = kEpiWarps * 4096;
   static constexpr uint32_t SMEM = STAGES * STAGE + EPI + 1024 + 256;
   static_assert(BN % 16 == 0 && BN >= 32 && BN <= 256, "UMMA N for M=256");
   static_assert(B_BYTES % 1024 == 0, "1024-byte aligned stages (SW128 atoms)");
@@ -82,7 +85,7 @@ k_gemm2_tf32x3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     }
     for (int a = 0; a < 2; ++a) {
       tc::mbar_init(&tfull[a], 1);
-      tc::mbar_init(&tempty[a], group_count);
+      tc::mbar_init(&tempty[a], 2);   // one arrival per CTA (after the epilogue barrier)
     }
     tc::fence_mbar_init();
     tc::tma_prefetch(&tmA);
@@ -182,26 +185,26 @@ k_gemm2_tf32x3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         if (++s == S) { s = 0; ph ^= 1; }
       }
     }
-  } else {  // ---------------- epilogue (128 threads per CTA, its own 128 rows)
+  } else {  // ---------------- epilogue (256 threads per CTA, its own 128 rows)
     const int q = warp & 3;
+    const int half = (warp - 6) >> 2;
+    constexpr int kSplit = ((BN + 1) / 2 + 31) / 32 * 32;
+    const int c_beg = half ? kSplit : 0, c_end = half ? BN : (kSplit < BN ? kSplit : BN);
     const uint32_t tempty0 = tc::mapa(tc::smem_u32(tempty), 0);
-    float4* stg = reinterpret_cast<float4*>(epi + q * 4096);
+    float4* stg = reinterpret_cast<float4*>(epi + (warp - 6) * 4096);
     int acc = 0;
     uint32_t aph = 0;
     for (int64_t t = pair; t < n_tiles; t += npairs) {   // n_tiles_n == 1 (BN >= N)
       const int64_t m0 = t * 2 * kBM + rank * kBM;
       const int64_t tn = t + npairs;
-      epi_prefetch_next<BN>(e, tn < n_tiles ? tn * 2 * kBM + rank * kBM : -1, threadIdx.x % 128);
+      if (half == 0)
+        epi_prefetch_next<BN>(e, tn < n_tiles ? tn * 2 * kBM + rank * kBM : -1, threadIdx.x % 128);
       tc::mbar_wait(&tfull[acc], aph);
       tc::tc_fence_after();
-      epi_tile<BN>(e, tmem_base + acc * G::ACC, stg, m0, q, lane);
+      epi_tile<BN>(e, tmem_base + acc * G::ACC, stg, m0, q, lane, c_beg, c_end);
       tc::tc_fence_before();
-      if (single) {
-        asm volatile("bar.sync 2, 128;" ::: "memory");
-        if (threadIdx.x % 128 == 0) tc::mbar_arrive_cluster(tempty0 + acc * 8);
-      } else {
-        tc::mbar_arrive_cluster(tempty0 + acc * 8);
-      }
+      asm volatile("bar.sync 2, 256;" ::: "memory");   // all 8 epilogue warps
+      if (warp == 6 && lane == 0) tc::mbar_arrive_cluster(tempty0 + acc * 8);
       acc ^= 1;
       if (acc == 0) aph ^= 1;
     }

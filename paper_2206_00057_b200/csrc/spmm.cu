@@ -384,18 +384,9 @@ digest_status launch_mb(const SpmmArgs& a, cudaStream_t s, int64_t blocks, doubl
     const char* e = getenv("DIGEST_SPMM_PFH");
     pfh = e ? atoi(e) : 0;
   }
-  static int xr = -1;   // DIGEST_SPMM_XR=1: cross-row pipelining in the prefetching kernel
-  if (xr < 0) {
-    const char* e = getenv("DIGEST_SPMM_XR");
-    xr = e ? atoi(e) : 0;
-  }
-  if (PF && xr) {
-    static const int64_t cap = resident_ctas(k_spmm<LC, VPL, UNR, true, MB, false>);
-    if (spmm_persistent(a) && blocks > cap) blocks = cap;
-    DG_LAUNCH_TAG(DIGEST_PROF_SPMM, a.full_width > 0 ? a.full_width : a.width, s, bytes, flops,
-                  (k_spmm<LC, VPL, UNR, true, MB, false>),
-                  (unsigned)blocks, 256, 0, a);
-  } else if (PF && pfh && a.hints) {
+  // (cross-row pipelining, the kernel's XR=true form, measured 20-50% slower with the
+  // persistent grid -- profiles/r1_spmm_variant_sweep.log -- and is not instantiated)
+  if (PF && pfh && a.hints) {
     static const int64_t cap = resident_ctas(k_spmm<LC, VPL, UNR, false, MB, true>);
     if (spmm_persistent(a) && blocks > cap) blocks = cap;
     DG_LAUNCH_TAG(DIGEST_PROF_SPMM, a.full_width > 0 ? a.full_width : a.width, s, bytes, flops,
@@ -436,10 +427,9 @@ digest_status launch(const SpmmArgs& a, cudaStream_t s) {
     const char* e = getenv("DIGEST_SPMM_MB");
     mb = e ? atoi(e) : 0;
   }
+  // (MB 5 and 6 were measured slower for every width and are not instantiated)
   switch (mb ? mb : MB_DEFAULT) {
     case 4: return launch_mb<LC, VPL, UNR, PF, 4>(a, s, blocks, bytes, flops);
-    case 5: return launch_mb<LC, VPL, UNR, PF, 5>(a, s, blocks, bytes, flops);
-    case 6: return launch_mb<LC, VPL, UNR, PF, 6>(a, s, blocks, bytes, flops);
     default: return launch_mb<LC, VPL, UNR, PF, 1>(a, s, blocks, bytes, flops);
   }
   return DIGEST_OK;

@@ -58,3 +58,25 @@ def test_no_cpu_fallback_in_product_path():
         if f.endswith(".py"):
             txt = open(os.path.join(pkg, f)).read()
             assert "import oracle" not in txt and "from oracle" not in txt, f
+
+
+def test_peer_and_ps_argument_errors():
+    """Peer transport, stale-store export and DIGEST-A PS calls reject bad arguments before
+    touching the device."""
+    from paper_2206_00057_b200 import capi as D
+    L = D.lib
+    out = C.c_void_p()
+    assert L.digest_comm_init_peer(0, 0, 16, C.byref(out)) == 1          # nranks = 0
+    assert L.digest_comm_init_peer(2, 2, 16, C.byref(out)) == 1          # rank out of range
+    assert L.digest_comm_init_peer(2, 0, -1, C.byref(out)) == 1          # negative window
+    assert L.digest_comm_export(None, None) == 1
+    assert L.digest_comm_connect(None, None) == 1
+    n = C.c_size_t()
+    assert L.digest_store_export(None, None, C.byref(n)) == 1
+    assert L.digest_store_connect(None, None, 0) == 1
+    assert L.digest_ps_mix(None, None, 4, 0.5, None) == 1
+    buf = (C.c_float * 4)()
+    assert L.digest_ps_mix(buf, buf, 4, 0.0, None) == 1                 # alpha outside (0, 1]
+    assert L.digest_ps_upload_peer(None, None, 4, 0.5, None) == 3        # no connected window
+    assert L.digest_delay(-1, None) == 1
+    assert L.digest_store_create_ex(None, None, 0, None, 0, C.byref(out)) == 1

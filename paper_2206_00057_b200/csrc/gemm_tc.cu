@@ -47,6 +47,36 @@ bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t out
   return r == CUDA_SUCCESS;
 }
 
+// Row-gather map for TMA tile::gather4: fp32 [outer rows x inner floats], box = one row of
+// `inner` floats (no swizzle, rows land packed in shared memory).
+bool make_tmap_rows(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
+                    uint64_t row_stride_bytes) {
+  CUtensorMap probe;
+  if (!make_tmap_2d(&probe, base, inner, outer, row_stride_bytes, 32, 1)) return false;  // loads fn
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return false;
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_stride_bytes};
+  cuuint32_t box[2] = {(cuuint32_t)inner, 1};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+bool make_tmap_rows_fwd(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
+                        uint64_t row_stride_bytes) {
+  return make_tmap_rows(m, base, inner, outer, row_stride_bytes);
+}
+
 namespace {
 
 constexpr int kBM = 128, kBK = 32, kThreads = 320;

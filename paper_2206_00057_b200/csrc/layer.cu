@@ -97,6 +97,7 @@ dg::SpmmArgs spmm_full(const digest_part* p, const float* X0, int64_t ld0, const
   a.X0 = X0;
   a.ld0 = ld0;
   a.split = p->n_local;
+  a.x0_rows = p->n_local;
   a.X1 = X1;
   a.ld1 = ld1;
   a.Y = Y;
@@ -127,6 +128,7 @@ dg::SpmmArgs spmm_rh(const digest_part* p, const float* X, int64_t ld, float* Y,
   a.X0 = X;
   a.ld0 = ld;
   a.split = INT64_MAX;
+  a.x0_rows = p->n_local;
   a.X1 = X;
   a.ld1 = ld;
   a.Y = Y;

@@ -6,9 +6,15 @@
 // independent row gathers in flight per edge group (memory-level parallelism).
 // Halo rows come from a second pointer (no copy of the stale store into a
 // contiguous X_ext).  HBM-bound: ~2 flop per (8 + 4w) bytes per nonzero.
+#include <cudaTypedefs.h>
+
 #include "kernels.cuh"
+#include "tc_util.cuh"
 
 namespace dg {
+// gemm_tc.cu: TMA map for tile::gather4 row copies of an fp32 [outer x inner] matrix
+bool make_tmap_rows_fwd(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
+                        uint64_t row_stride_bytes);
 namespace {
 
 // L2 cache policies: the gathered source rows are re-read by many rows (keep them),
@@ -343,6 +349,207 @@ __global__ void __launch_bounds__(256, MB) k_spmm_rt(SpmmArgs a) {
 }
 
 
+// Single-source product through TMA row gathers (tile::gather4), experimental
+// (DIGEST_SPMM_TMA=1; measured 1.45-1.6x SLOWER than the load-based kernels at w=48/100,
+// products M=1 and 8 parts -- profiles/r1_spmm_variant_sweep.log -- so it is off).  Warp per row as above, but the 32 gathered rows of a (col, val)
+// chunk are fetched by ceil(cnt/4) gather4 copies that one lane issues into a per-warp
+// shared-memory buffer (two buffers: the next chunk -- possibly of the next row -- is in
+// flight while the current one is consumed), so no registers are tied up by loads in
+// flight and the row_ptr -> col -> gather chain of the next row overlaps this row.
+__device__ __forceinline__ void gather4(void* dst, const CUtensorMap* m, uint64_t* bar, int32_t r0,
+                                        int32_t r1, int32_t r2, int32_t r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(tc::smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(tc::smem_u32(bar)), "r"(0), "r"(r0), "r"(r1),
+      "r"(r2), "r"(r3)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait_bounded(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = tc::smem_u32(bar);
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}"
+        : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+    if (ok) return;
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 10ull * 1000000000ull) __trap();
+  }
+}
+
+template <int LC, int VPL>
+__global__ void __launch_bounds__(256) k_spmm_tg(SpmmArgs a, const __grid_constant__ CUtensorMap tm,
+                                                 int slot_bytes) {
+  constexpr int EG = 32 / LC;
+  extern __shared__ __align__(128) uint8_t smem_tg[];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw_cta = blockDim.x >> 5;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_tg) + wib * 2;
+  int32_t* idx = reinterpret_cast<int32_t*>(smem_tg + 1024) + wib * 32;
+  uint8_t* ring = smem_tg + 2048 + (size_t)wib * 16 * slot_bytes;
+  if (lane == 0) {
+    tc::mbar_init(&bar[0], 1);
+    tc::mbar_init(&bar[1], 1);
+    tc::fence_mbar_init();
+  }
+  __syncwarp();
+  const int cl = lane % LC, g = lane / LC, w4 = a.width >> 2;
+  const int row_bytes = a.width * 4;
+  const int64_t nwarps = (int64_t)gridDim.x * nw_cta;
+  int64_t irow = (int64_t)blockIdx.x * nw_cta + wib, ie0 = 0, iend = 0;
+  if (irow < a.n_rows) {
+    ie0 = a.row_ptr[irow];
+    iend = a.in_len ? ie0 + a.in_len[irow] : a.row_ptr[irow + 1];
+  }
+  int64_t crow[2] = {0, 0};
+  int ccnt[2] = {0, 0};
+  bool clast[2] = {false, false};
+  float v0 = 0.f, v1 = 0.f;
+  uint32_t ph0 = 0, ph1 = 0;
+  float4 acc[VPL];
+#pragma unroll
+  for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+
+  auto issue = [&](int b) -> bool {
+    if (irow >= a.n_rows) return false;
+    const int64_t e0 = ie0;
+    const int cnt = (int)min((int64_t)32, iend - e0);
+    int32_t c = 0;
+    float v = 0.f;
+    if (lane < cnt) {
+      c = __ldg(a.col + e0 + lane) & 0x7fffffff;
+      v = __ldg(a.val + e0 + lane);
+    } else if (cnt > 0) {
+      c = __ldg(a.col + e0) & 0x7fffffff;   // pad a gather4 group with a row already fetched
+    }
+    crow[b] = irow;
+    ccnt[b] = cnt;
+    if (b) v1 = v; else v0 = v;
+    ie0 += 32;
+    clast[b] = ie0 >= iend;
+    if (clast[b]) {
+      irow += nwarps;
+      if (irow < a.n_rows) {
+        ie0 = a.row_ptr[irow];
+        iend = a.in_len ? ie0 + a.in_len[irow] : a.row_ptr[irow + 1];
+      }
+    }
+    if (cnt > 0) {
+      idx[lane] = c;
+      __syncwarp();
+      if (lane == 0) {
+        const int ng = (cnt + 3) >> 2;
+        tc::mbar_arrive_expect_tx(&bar[b], (uint32_t)(ng * 4 * row_bytes));
+        uint8_t* dst = ring + (size_t)b * 8 * slot_bytes;
+        for (int q = 0; q < ng; ++q)
+          gather4(dst + (size_t)q * slot_bytes, &tm, &bar[b], idx[4 * q], idx[4 * q + 1],
+                  idx[4 * q + 2], idx[4 * q + 3]);
+      }
+      __syncwarp();
+    }
+    return true;
+  };
+
+  auto consume = [&](int b) {
+    const int cnt = ccnt[b];
+    if (cnt > 0) {
+      if (b) { mbar_wait_bounded(&bar[1], ph1); ph1 ^= 1; }
+      else   { mbar_wait_bounded(&bar[0], ph0); ph0 ^= 1; }
+    }
+    const float v = b ? v1 : v0;
+    const uint8_t* base = ring + (size_t)b * 8 * slot_bytes;
+#pragma unroll 4
+    for (int j0 = 0; j0 < 32; j0 += EG) {
+      if (j0 >= cnt) break;
+      const int j = j0 + g;
+      const float x = __shfl_sync(0xffffffffu, v, j & 31);
+      if (g < EG && j < cnt) {
+        const float* rowp = reinterpret_cast<const float*>(base + (size_t)(j >> 2) * slot_bytes +
+                                                           (size_t)(j & 3) * row_bytes);
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) {
+          const int i4 = cl + q * LC;
+          if (i4 < w4) {
+            const float4 t = reinterpret_cast<const float4*>(rowp)[i4];
+            acc[q].x = fmaf(x, t.x, acc[q].x);
+            acc[q].y = fmaf(x, t.y, acc[q].y);
+            acc[q].z = fmaf(x, t.z, acc[q].z);
+            acc[q].w = fmaf(x, t.w, acc[q].w);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // reads before the next fill
+    if (clast[b]) {
+#pragma unroll
+      for (int off = LC; off < EG * LC; off <<= 1)
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) {
+          const bool in = lane + off < EG * LC;
+          const float x = __shfl_down_sync(0xffffffffu, acc[q].x, off);
+          const float y = __shfl_down_sync(0xffffffffu, acc[q].y, off);
+          const float z = __shfl_down_sync(0xffffffffu, acc[q].z, off);
+          const float w = __shfl_down_sync(0xffffffffu, acc[q].w, off);
+          if (in) {
+            acc[q].x += x;
+            acc[q].y += y;
+            acc[q].z += z;
+            acc[q].w += w;
+          }
+        }
+      spmm_row_epilogue<LC, VPL>(a, crow[b], lane, cl, g, w4, acc);
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+
+  int b = 0;
+  bool have = issue(0);
+  while (have) {
+    const bool next = issue(b ^ 1);
+    consume(b);
+    b ^= 1;
+    have = next;
+  }
+}
+
+template <int LC, int VPL>
+digest_status launch_tg(const SpmmArgs& a, cudaStream_t s) {
+  CUtensorMap tm;
+  DG_ARG(make_tmap_rows_fwd(&tm, a.X0, (uint64_t)a.width, (uint64_t)a.x0_rows,
+                            (uint64_t)a.ld0 * 4),
+         DIGEST_E_CUDA, "row-gather tensor map failed");
+  const int slot = (int)round_up(4 * (int64_t)a.width * 4, 128);
+  int wpc = (int)((227 * 1024 - 2048) / (16 * (int64_t)slot));
+  if (wpc > 8) wpc = 8;
+  if (wpc < 1) wpc = 1;
+  const int smem = 2048 + wpc * 16 * slot;
+  static int attr = 0;
+  if (smem > attr) {
+    DG_CUDA(cudaFuncSetAttribute(k_spmm_tg<LC, VPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem));
+    attr = smem;
+  }
+  int per_sm = 0;
+  DG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmm_tg<LC, VPL>, wpc * 32, smem));
+  int64_t blocks = (int64_t)(per_sm < 1 ? 1 : per_sm) * num_sms();
+  const int64_t need = ceil_div(a.n_rows, wpc);
+  if (blocks > need) blocks = need < 1 ? 1 : need;
+  const double W = a.full_width > 0 ? a.full_width : a.width;
+  const double frac = a.width / W;
+  const double bytes = frac * ((double)a.nnz * (8.0 + 4.0 * W) + (double)a.n_rows * (4.0 * W + 8.0));
+  const double flops = 2.0 * (double)a.nnz * a.width;
+  DG_LAUNCH_TAG(DIGEST_PROF_SPMM, a.full_width > 0 ? a.full_width : a.width, s, bytes, flops,
+                (k_spmm_tg<LC, VPL>), (unsigned)blocks, wpc * 32, smem, a, tm, slot);
+  return DIGEST_OK;
+}
+
 // Grid: at most the number of CTAs that are resident at once (a persistent grid).  The
 // rows are dealt round-robin (row = warp + k * nwarps), so with every warp resident the
 // rows in flight form one narrow, monotonically advancing window -- a graph block's
@@ -495,6 +702,18 @@ digest_status spmm(const SpmmArgs& a0, cudaStream_t s) {
 
 digest_status spmm_one(const SpmmArgs& a, cudaStream_t s) {
   const int w4 = a.width / 4;
+  static int tg = -1;   // DIGEST_SPMM_TMA=1: TMA row-gather kernel for single-source products
+  if (tg < 0) {
+    const char* e = getenv("DIGEST_SPMM_TMA");
+    tg = e ? atoi(e) : 0;
+  }
+  const bool single = a.in_len != nullptr || a.X1 == nullptr || a.split >= INT32_MAX;
+  if (tg && single && a.x0_rows > 0 && a.x0_rows < INT32_MAX && a.width <= 256 &&
+      (a.width * 4) % 16 == 0) {
+    if (w4 <= 12) return launch_tg<4, 3>(a, s);
+    if (w4 <= 32) return launch_tg<8, 4>(a, s);
+    return launch_tg<32, 2>(a, s);
+  }
   // (lanes per edge, float4 per lane, edges per group per step); EG = 32 / LC edge groups
   if (w4 <= 1) return launch<1, 1, 1>(a, s);
   if (w4 <= 2) return launch<2, 1, 1>(a, s);

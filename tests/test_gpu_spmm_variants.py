@@ -25,6 +25,9 @@ CASES += [(256, {"DIGEST_SPMM_SLAB": "64"}), (256, {"DIGEST_SPMM_HINTS": "0"}),
           (256, {"DIGEST_SPMM_GRID": "0"}), (100, {"DIGEST_SPMM_SLAB": "32"})]
 CASES += [(w, {}) for w in (4, 8, 16, 32, 64, 128, 384, 512, 1024)]
 CASES += [(128, {"DIGEST_SPMM_V32": "1"})]
+# TMA row-gather kernel (single-source products): P_in (mode 1) and P_out^T (mode 2)
+CASES += [(w, {"DIGEST_SPMM_TMA": "1", "MODE": m}) for w in (4, 16, 48, 100, 128, 256)
+          for m in ("1", "2")]
 CASES += [(w, {"DIGEST_SPMM_MB": mb}) for w in (48, 100, 256) for mb in ("1", "4")]
 
 
@@ -35,12 +38,20 @@ def test_spmm_variant(width, env, tmp_path):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     out = str(tmp_path / "y.npz")
+    env = dict(env)
+    mode = int(env.pop("MODE", "0"))
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "spmm_variant_proc.py"), out,
-                        str(width), "5"], env={**os.environ, **env, "PYTHONPATH": ROOT},
+                        str(width), "5", str(mode)], env={**os.environ, **env, "PYTHONPATH": ROOT},
                        capture_output=True, text=True, timeout=280)
     assert r.returncode == 0, r.stderr[-2000:]
     d = np.load(out)
     op = oracle.oracle_partition(d["ip"], d["ix"], d["part"], 3, 1)
-    ref = layer_forward(op, d["xl"], d["xh"], np.eye(width), relu=False)["A"]
+    if mode == 0:
+        ref = layer_forward(op, d["xl"], d["xh"], np.eye(width), relu=False)["A"]
+    else:
+        from oracle.gcn import prop_matrix
+        P = prop_matrix(op)
+        P_in, P_out = P[:, :op.n_local], P[:, op.n_local:]
+        ref = (P_in @ d["xl"]) if mode == 1 else (P_out.T @ d["xl"])
     err = np.abs(d["y"] - ref).max() / np.abs(ref).max()
     assert err <= 1e-4, err

@@ -729,6 +729,9 @@ digest_status spmm_one(const SpmmArgs& a, cudaStream_t s) {
     if (v == 2) return launch<4, 3, 2, false>(a, s);
     if (v == 3) return launch<4, 3, 4, false>(a, s);
     if (v == 4) return launch<8, 2, 2>(a, s);
+    if (v == 5) return launch<2, 6, 1, true, 4>(a, s);
+    if (v == 6) return launch<2, 6, 2, true>(a, s);
+    if (v == 7) return launch<4, 3, 1, true, 4>(a, s);
     // measured best for w=48 with the persistent grid (products M=1): 4.11 ms vs 4.30 ms
     // for <4,3,4> (profiles/r1_spmm_variant_sweep.log)
     return launch<4, 3, 2, true, 4>(a, s);

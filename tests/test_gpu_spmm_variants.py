@@ -17,7 +17,7 @@ from oracle.gcn import layer_forward
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
-CASES = [(48, {"DIGEST_SPMM_V12": str(v)}) for v in range(5)]
+CASES = [(48, {"DIGEST_SPMM_V12": str(v)}) for v in range(8)]
 CASES += [(48, {"DIGEST_SPMM_PFH": "1"}), (48, {"DIGEST_SPMM_GRID": "1"})]
 CASES += [(100, {"DIGEST_SPMM_V25": str(v)}) for v in range(6)]
 CASES += [(256, {"DIGEST_SPMM_V": str(v)}) for v in range(7)]

@@ -18,7 +18,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import oracle
-from paper_2206_00057_b200.dist import Schedule, broadcast_ids, check_exchange_plan
+from paper_2206_00057_b200.dist import (Schedule, all_gather_bytes, broadcast_ids,
+                                        check_exchange_plan, grad_count)
 from synth import make_inputs, make_block_parts, make_random_parts, small_config
 
 
@@ -73,8 +74,13 @@ def _worker(rank, world, port, random_parts, q):
         for k, b in bufs.items():
             halo[p.recv_off[k]:p.recv_off[k] + p.recv_count[k]] = b.numpy()
         exact = halo.tobytes() == H_global[p.halo_ids].tobytes()
-        # 3) id broadcast
+        # 3) id broadcast; the peer-transport handle exchange (rank-order blobs of any size,
+        #    including an empty blob from a rank whose window failed)
         ids = broadcast_ids(lambda: bytes(range(128)), 2, rank)
+        blobs = all_gather_bytes(bytes([rank]) * (64 + rank), world)
+        empty = all_gather_bytes(b"" if rank == world - 1 else b"x", world)
+        gather_ok = (blobs == [bytes([k]) * (64 + k) for k in range(world)] and
+                     empty[-1] == b"" and all(e == b"x" for e in empty[:-1]))
         # 4) AGG: sum of per-part gradients over ranks == oracle aggregated gradient
         run = oracle.oracle_train(inp.indptr, inp.indices, inp.x, inp.y, inp.train_mask,
                                   inp.weights, cfg.num_classes, part, world, sync_interval=1,
@@ -99,7 +105,8 @@ def _worker(rank, world, port, random_parts, q):
         dist.all_reduce(flat)
         agg = np.concatenate([gw.ravel() for gw in rec.grads])
         agg_ok = np.allclose(flat.numpy(), agg, rtol=1e-12, atol=1e-14)
-        q.put((rank, S.tolist(), bad_caught, exact, ids[0] == bytes(range(128)), agg_ok))
+        q.put((rank, S.tolist(), bad_caught, exact, ids[0] == bytes(range(128)) and gather_ok,
+               agg_ok))
     finally:
         dist.destroy_process_group()
 
@@ -131,3 +138,10 @@ def test_schedule_guards():
     assert s.counts(40, 2) == ((40 // 10) * 2, ((40 - 1) // 10 + 1) * 2)
     with pytest.raises(ValueError):
         Schedule(0)
+
+
+def test_grad_count_matches_the_flat_weight_layout():
+    """The peer window's AGG slot size: sum of d_l * d_{l+1} (the flat W / G buffers)."""
+    assert grad_count((100, 256, 256, 48)) == 100 * 256 + 256 * 256 + 256 * 48 == 103424
+    assert grad_count((604, 256, 48)) == 166912
+    assert grad_count((8, 4)) == 32

@@ -64,6 +64,10 @@ CASES = {
     "M3_N1_bf16_store": dict(world=3, parts_seed=3, epochs=4, graph=dict(GRAPH, seed=27),
                              train=dict(sync_interval=1, lr=0.05, optimizer="sgd",
                                         store_bf16=True)),
+    # row-L2-normalised pushes (Alg. 1, reading A9) through the fused put kernel
+    "M2_N1_normalized": dict(world=2, parts_seed=5, epochs=4, graph=dict(GRAPH, seed=28),
+                             train=dict(sync_interval=1, lr=0.05, optimizer="sgd",
+                                        normalize_pushed=True)),
 }
 
 
@@ -104,7 +108,8 @@ def test_peer_transport_multiprocess(name, tmp_path):
                               epochs=spec["epochs"], lr=tr["lr"], optimizer=tr["optimizer"],
                               mode="fresh" if tr.get("fresh") else "stale",
                               halo_grad="same_epoch" if tr.get("halo_grad") else "none",
-                              store_dtype="bf16" if tr.get("store_bf16") else "fp32")
+                              store_dtype="bf16" if tr.get("store_bf16") else "fp32",
+                              normalize_pushed=bool(tr.get("normalize_pushed")))
     tol = 5e-4 if tr.get("store_bf16") else TOL
     loss = res["loss"].sum(axis=0)
     for r, rec in enumerate(run.records):
@@ -128,6 +133,10 @@ ASYNC = {
                          delay_ms=150.0, train=dict(sync_interval=1, lr=0.05, optimizer="sgd")),
     "M4_adam_N2": dict(world=4, epochs=6, graph=dict(GRAPH, seed=33), straggler=3, delay_ms=50.0,
                        train=dict(sync_interval=2, lr=0.01, optimizer="adam")),
+    # DIGEST-A with the bf16 store: NOWAIT bf16 puts, seqlock SNAPSHOT widening pulls
+    "M3_bf16_store": dict(world=3, epochs=6, graph=dict(GRAPH, seed=34), straggler=0,
+                          delay_ms=100.0, train=dict(sync_interval=1, lr=0.05, optimizer="sgd",
+                                                     store_bf16=True)),
 }
 
 

@@ -39,6 +39,7 @@ class AsyncRecord:
     pushed: bool
     uploaded: list = field(default_factory=list)       # W_m uploaded (record_weights)
     halo_versions: dict = field(default_factory=dict)  # l -> event index of each halo row
+    halos: dict = field(default_factory=dict)          # l -> halo rows used (record_halos)
 
 
 @dataclass
@@ -53,7 +54,7 @@ class AsyncRun:
 
 def oracle_train_async(indptr, indices, x, y, train_mask, weights, num_classes, part_of,
                        num_parts, sync_interval, events, lr=0.01, optimizer="sgd", alpha=None,
-                       parts=None, record_weights=False) -> AsyncRun:
+                       parts=None, record_weights=False, record_halos=False) -> AsyncRun:
     if sync_interval < 1:
         raise ValueError("sync interval must be >= 1")
     M, Ns = num_parts, sync_interval
@@ -97,6 +98,8 @@ def oracle_train_async(indptr, indices, x, y, train_mask, weights, num_classes, 
             outs[l] = o
             if l < L:
                 rec.halo_versions[l] = hver[(l, m)].copy()
+                if record_halos:
+                    rec.halos[l] = halo[(l, m)].copy()
                 if push:                                   # visible to later events
                     committed[l][p.local_ids] = o["H"]
                     cver[l][p.local_ids] = ev

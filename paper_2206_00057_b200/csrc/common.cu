@@ -1,5 +1,6 @@
 // Status text, launch counting and live event profiling (digest.h "profiling").
 #include <atomic>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <mutex>
@@ -150,3 +151,13 @@ digest_status digest_prof_read_detail(int32_t max_groups, int32_t* cls_h, int32_
 }
 
 }  // extern "C"
+
+namespace dg {
+const char* knob(const char* name) {
+  static const bool on = [] {
+    const char* e = getenv("DIGEST_KNOBS");
+    return e && atoi(e) == 1;
+  }();
+  return on ? getenv(name) : nullptr;
+}
+}  // namespace dg

@@ -27,6 +27,11 @@ inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 inline int64_t ceil_div(int64_t x, int64_t m) { return (x + m - 1) / m; }
 int num_sms();
 
+// Experiment switches (kernel variants, schedules) read from the environment ONLY when
+// DIGEST_KNOBS=1 is set: the product path ignores the environment otherwise.  Returns
+// getenv(name) or NULL.
+const char* knob(const char* name);
+
 }  // namespace dg
 
 #define DG_ARG(cond, status, ...)                                  \

@@ -316,7 +316,7 @@ digest_status gemm_tc2(const GemmArgs& g, const float* hi, const float* lo, int 
 bool gemm_tc_eligible(const GemmArgs& g) {
   static int force_simt = -1;
   if (force_simt < 0) {
-    const char* e = getenv("DIGEST_GEMM");
+    const char* e = dg::knob("DIGEST_GEMM");
     force_simt = (e && e[0] == 's') ? 1 : 0;
   }
   if (force_simt) return false;

@@ -248,7 +248,7 @@ digest_status launch2(const GemmArgs& g, const CUtensorMap& tA, const CUtensorMa
   Launch L(DIGEST_PROF_GEMM, s, bytes, flops, 30000000 + (int)g.K * 1000 + g.N);
   static int single = -1;   // DIGEST_GEMM_SINGLE_ARRIVE (default 1)
   if (single < 0) {
-    const char* ev = getenv("DIGEST_GEMM_SINGLE_ARRIVE");
+    const char* ev = dg::knob("DIGEST_GEMM_SINGLE_ARRIVE");
     single = ev ? atoi(ev) : 1;
   }
   cudaError_t e = cudaLaunchKernelEx(&cfg, k_gemm2_tf32x3<BN>, tA, tBh, tBl, epi_of(g), (int)g.K,
@@ -265,7 +265,7 @@ digest_status launch2(const GemmArgs& g, const CUtensorMap& tA, const CUtensorMa
 bool gemm_tc2_enabled(int N, int K) {
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("DIGEST_GEMM_2CTA");
+    const char* e = dg::knob("DIGEST_GEMM_2CTA");
     v = e ? atoi(e) : 1;
   }
   // measured (tools/gemm_bench.py, 2.45M rows): N=256 1.64 -> 1.60 ms with pairs; N=48 is

@@ -51,16 +51,18 @@ digest_status make_plan(const digest_part* p, int32_t d_in, int32_t d_out, int32
   pl->ldi = round_up(d_in, 4);
   pl->ldo = round_up(d_out, 4);
   const size_t f = sizeof(float);
+  // every scratch sub-buffer is carved with the same 256-byte rounding as carve()
+  auto r = [](size_t b) { return (size_t)round_up((int64_t)b, 256); };
   size_t wg = dg::wgrad_scratch_bytes(pl->n + pl->h, d_in, d_out);
   pl->ldmb = round_up((d_out + 31) / 32, 4);
   if (pl->agg_first) {
     pl->saved = f * pl->n * pl->ldi;
-    size_t bwd = f * pl->n * pl->ldo + f * pl->n * pl->ldi + wg;
+    size_t bwd = r(f * pl->n * pl->ldo) + r(f * pl->n * pl->ldi) + wg;
     pl->scratch = bwd;
   } else {
     pl->saved = 0;
-    size_t fwd = f * (pl->n + pl->h) * pl->ldo;
-    size_t bwd = f * pl->n * pl->ldo + f * (pl->n + pl->h) * pl->ldo + wg;
+    size_t fwd = r(f * (pl->n + pl->h) * pl->ldo);
+    size_t bwd = r(f * pl->n * pl->ldo) + r(f * (pl->n + pl->h) * pl->ldo) + wg;
     pl->scratch = fwd > bwd ? fwd : bwd;
   }
   // saved = [A (AGG_FIRST) | 1-bit ReLU mask of H, n x ldmb words]

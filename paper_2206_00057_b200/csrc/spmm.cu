@@ -572,7 +572,7 @@ int64_t resident_ctas(K kern) {
 bool spmm_persistent(const SpmmArgs& a) {
   static int v = -2;
   if (v == -2) {
-    const char* e = getenv("DIGEST_SPMM_GRID");
+    const char* e = dg::knob("DIGEST_SPMM_GRID");
     v = e ? atoi(e) : -1;
   }
   if (v >= 0) return v == 0;
@@ -588,7 +588,7 @@ digest_status launch_mb(const SpmmArgs& a, cudaStream_t s, int64_t blocks, doubl
   // 0.454 ms; profiles/r1_spmm_variant_sweep.log)
   static int pfh = -1;
   if (pfh < 0) {
-    const char* e = getenv("DIGEST_SPMM_PFH");
+    const char* e = dg::knob("DIGEST_SPMM_PFH");
     pfh = e ? atoi(e) : 0;
   }
   // (cross-row pipelining, the kernel's XR=true form, measured 20-50% slower with the
@@ -631,7 +631,7 @@ digest_status launch(const SpmmArgs& a, cudaStream_t s) {
   // compiler's choice); the narrow widths are latency-bound and gain from occupancy
   static int mb = -1;
   if (mb < 0) {
-    const char* e = getenv("DIGEST_SPMM_MB");
+    const char* e = dg::knob("DIGEST_SPMM_MB");
     mb = e ? atoi(e) : 0;
   }
   // (MB 5 and 6 were measured slower for every width and are not instantiated)
@@ -653,7 +653,7 @@ digest_status spmm_one(const SpmmArgs& a, cudaStream_t s);
 int spmm_slab_width(const SpmmArgs& a) {
   static int env = -2;
   if (env == -2) {
-    const char* e = getenv("DIGEST_SPMM_SLAB");
+    const char* e = dg::knob("DIGEST_SPMM_SLAB");
     env = e ? atoi(e) : -1;
   }
   if (env >= 0) return env;
@@ -669,14 +669,14 @@ digest_status spmm(const SpmmArgs& a0, cudaStream_t s) {
   // (profiles/r1_spmm_variant_sweep.log).
   static int hints = -2;
   if (hints == -2) {
-    const char* e = getenv("DIGEST_SPMM_HINTS");
+    const char* e = dg::knob("DIGEST_SPMM_HINTS");
     hints = e ? atoi(e) : -1;
   }
   SpmmArgs a = a0;
   a.hints = hints >= 0 ? hints : (a0.width >= 128 ? 2 : 0);
   static int cs = -1;   // DIGEST_SPMM_STREAM_OUT: st.global.cs for the output rows
   if (cs < 0) {
-    const char* e = getenv("DIGEST_SPMM_STREAM_OUT");
+    const char* e = dg::knob("DIGEST_SPMM_STREAM_OUT");
     cs = e ? atoi(e) : 0;
   }
   a.stream_out = cs;
@@ -704,7 +704,7 @@ digest_status spmm_one(const SpmmArgs& a, cudaStream_t s) {
   const int w4 = a.width / 4;
   static int tg = -1;   // DIGEST_SPMM_TMA=1: TMA row-gather kernel for single-source products
   if (tg < 0) {
-    const char* e = getenv("DIGEST_SPMM_TMA");
+    const char* e = dg::knob("DIGEST_SPMM_TMA");
     tg = e ? atoi(e) : 0;
   }
   const bool single = a.in_len != nullptr || a.X1 == nullptr || a.split >= INT32_MAX;
@@ -722,7 +722,7 @@ digest_status spmm_one(const SpmmArgs& a, cudaStream_t s) {
   if (w4 <= 12) {
     static int v = -1;
     if (v < 0) {
-      const char* e = getenv("DIGEST_SPMM_V12");
+      const char* e = dg::knob("DIGEST_SPMM_V12");
       v = e ? atoi(e) : 0;
     }
     if (v == 1) return launch<4, 3, 4>(a, s);
@@ -740,7 +740,7 @@ digest_status spmm_one(const SpmmArgs& a, cudaStream_t s) {
   if (w4 <= 25) {   // w = 100 (products d0); variant 1: 6 groups x 5 lanes x 5 float4
     static int v = -1;
     if (v < 0) {
-      const char* e = getenv("DIGEST_SPMM_V25");
+      const char* e = dg::knob("DIGEST_SPMM_V25");
       v = e ? atoi(e) : 0;
     }
     if (v == 1) return launch<5, 5, 2, false>(a, s);
@@ -756,7 +756,7 @@ digest_status spmm_one(const SpmmArgs& a, cudaStream_t s) {
   if (w4 <= 32) {   // w = 128 (arxiv d0)
     static int v = -1;
     if (v < 0) {
-      const char* e = getenv("DIGEST_SPMM_V32");
+      const char* e = dg::knob("DIGEST_SPMM_V32");
       v = e ? atoi(e) : 0;
     }
     if (v == 1) return launch<8, 4, 2, false>(a, s);
@@ -765,7 +765,7 @@ digest_status spmm_one(const SpmmArgs& a, cudaStream_t s) {
   if (w4 <= 64) {
     static int v = -1;
     if (v < 0) {
-      const char* e = getenv("DIGEST_SPMM_V");
+      const char* e = dg::knob("DIGEST_SPMM_V");
       v = e ? atoi(e) : 0;
     }
     switch (v) {

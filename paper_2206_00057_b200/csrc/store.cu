@@ -38,6 +38,11 @@ struct Level {
   float* ret_recv = nullptr;    // n_send x ld: returned gradients received from peers (NCCL)
   int64_t last_pull = 0;        // epoch of the last pull call (peer transport)
   int64_t gseq = 0;             // grad_buffer calls so far (peer transport)
+  // Single-process (linked) stores: pushes that peers wrote into THIS store's back
+  // buffer (the receiver's own record; a pusher's version says nothing about what the
+  // receiver holds when workers push at different local epochs, DIGEST-A) and the
+  // count the last pull consumed.
+  int64_t rx_seq = 0, rx_seen = 0;
   size_t halo_bytes = 0;        // bytes of one n_halo x ld fp32 buffer
   bool bf16 = false;            // back buffer (and transfers) in bf16
   size_t es() const { return bf16 ? 2 : 4; }   // element size of back / send buffers
@@ -497,6 +502,7 @@ digest_status digest_push_boundary(digest_store* st, int32_t level, const float*
       Level& Lk = pk->lev[level - 1];
       DG_ARG(Lk.bf16 == L->bf16, DIGEST_E_STATE, "linked stores disagree on the bf16 store");
       sg.dst[k] = xrow(Lk.buf[1 - Lk.front], pk->part->recv_off[me], Lk.ld, Lk.es());
+      if (p->send_count[k] > 0) ++Lk.rx_seq;   // k's back buffer now holds new rows of mine
     }
     sg.start[M] = p->n_send;
     DG_TRY(pack(H_local, ld, p->send_idx, p->n_send, sg, L->ld, L->width, norm, s, L->bf16));
@@ -556,7 +562,9 @@ digest_status digest_pull(digest_store* st, int32_t level, int64_t epoch, int32_
     L->last_pull = epoch;
   }
   if (peer && mode == DIGEST_PULL_SNAPSHOT) {   // DIGEST-A: no waiting for arrivals
-    if (L->ver[back] > L->ver[L->front]) {
+    // Always copy: the owners push at their own pace, so whether new rows arrived is
+    // only known to the seqlock words, not to this rank's own push count.
+    {
       const digest_part* p = st->part;
       SnapSegs sg{};
       int n = 0;
@@ -578,7 +586,12 @@ digest_status digest_pull(digest_store* st, int32_t level, int64_t epoch, int32_
     if (front_h) *front_h = L->buf[L->front];
     return DIGEST_OK;
   }
-  if (L->ver[back] > L->ver[L->front]) {
+  // new rows in the back buffer: our own schedule's push (every rank pushes at the same
+  // epochs in the synchronous mode), or -- linked single-process stores -- rows a peer
+  // wrote there since the last pull (DIGEST-A: peers push at their own local epochs)
+  const bool fresh_rows = L->ver[back] > L->ver[L->front] || (!peer && mode == DIGEST_PULL_COPY && L->rx_seq > L->rx_seen);
+  L->rx_seen = L->rx_seq;
+  if (fresh_rows) {
     if (peer) {   // wait until every owner's rows of this version have arrived
       dg::FlagWait arr{};
       arr.value = L->ver[back];

@@ -318,7 +318,7 @@ __global__ void k_wgrad_reduce(const float* __restrict__ partial, int nz, int MT
 int wgrad_dbg() {
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("DIGEST_WGRAD_DBG");   // timing experiments only (wrong results)
+    const char* e = dg::knob("DIGEST_WGRAD_DBG");   // timing experiments only (wrong results)
     v = e ? atoi(e) : 0;
   }
   return v;
@@ -385,7 +385,7 @@ size_t wgrad_tc_scratch_bytes(int32_t M, int32_t N) {
 }
 
 bool wgrad_tc_eligible(const WgradSeg* segs, int nseg, int M, int N) {
-  const char* e = getenv("DIGEST_GEMM");
+  const char* e = dg::knob("DIGEST_GEMM");
   if (e && e[0] == 's') return false;
   if (N > 256 || N % 4 || M % 4 || M < 8) return false;
   for (int i = 0; i < nseg; ++i) {

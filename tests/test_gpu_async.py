@@ -21,6 +21,11 @@ def _cuda():
     torch.cuda.set_device(0)
 
 
+def read_rows(addr, n, ld, width):
+    from tests.test_gpu_parity import read_rows as rr
+    return rr(addr, n, ld, width)
+
+
 def rel(got, ref):
     got, ref = np.asarray(got, np.float64), np.asarray(ref, np.float64)
     return np.abs(got - ref).max() / np.abs(ref).max()
@@ -45,12 +50,26 @@ def test_async_loopback_vs_oracle(M, N, opt, straggler):
     grp = AsyncLoopbackGroup(ws)
     run = oracle_train_async(inp.indptr, inp.indices, inp.x, inp.y, inp.train_mask, inp.weights,
                              cfg.num_classes, part, M, sync_interval=N, events=ev, lr=lr,
-                             optimizer=opt)
+                             optimizer=opt, record_halos=True)
     for j, m in enumerate(ev):
         grp.event(m)
         torch.cuda.synchronize()
-        got, ref = ws[m].loss.item(), run.records[j].loss
+        rec = run.records[j]
+        got, ref = ws[m].loss.item(), rec.loss
         assert abs(got - ref) <= TOL * abs(ref), (j, m, got, ref)
+        # the halo rows the event used, row by row: never-pushed rows (version -1) are
+        # exactly zero, the others are the owner's latest push before the pull
+        for l, hv in rec.halo_versions.items():
+            if ws[m].part.n_halo == 0:
+                continue
+            p, ld, _ = D.digest_store_front(ws[m].store, l)
+            front = read_rows(p, ws[m].part.n_halo, ld, cfg.dims[l]).cpu().numpy()
+            cold = hv < 0
+            assert not front[cold].any(), (j, m, l, "rows never pushed must be zero")
+            if (~cold).any():
+                h = rec.halos[l][~cold]
+                err = np.abs(front[~cold] - h).max() / max(np.abs(h).max(), 1e-30)
+                assert err <= TOL, (j, m, l, err)
     wref = np.concatenate([w.ravel() for w in run.weights])
     assert rel(grp.W_global.cpu().numpy(), wref) <= TOL
     assert grp.ps_updates == M * R

@@ -41,7 +41,7 @@ def test_spmm_variant(width, env, tmp_path):
     env = dict(env)
     mode = int(env.pop("MODE", "0"))
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "spmm_variant_proc.py"), out,
-                        str(width), "5", str(mode)], env={**os.environ, **env, "PYTHONPATH": ROOT},
+                        str(width), "5", str(mode)], env={**os.environ, **env, "DIGEST_KNOBS": "1", "PYTHONPATH": ROOT},
                        capture_output=True, text=True, timeout=280)
     assert r.returncode == 0, r.stderr[-2000:]
     d = np.load(out)

@@ -3,7 +3,8 @@
     python tools/spmm_bench.py [--config products] [--parts 1] [--rank 0] [--width 256]
                                [--iters 5] [--mode 0]
 Prints per-launch ms, GTEPS and edge-gather GB/s (the SURVEY §8.d.4 byte model).
-Variants are selected through the library's env vars (DIGEST_SPMM_SLAB, ...).
+Variants are selected through the library's experiment switches (DIGEST_KNOBS=1 plus
+DIGEST_SPMM_SLAB, ...).
 """
 import argparse
 import json

@@ -49,8 +49,10 @@ def layer_backward(part, x_local, x_halo, w, g_out, act_mask, need_g_in: bool,
     implementation's ReLU decisions (integer decisions taken once, in one precision).
 
     need_g_halo: also return G_halo = P_out^T D W^T (n_halo rows), the gradient this
-    partition's rows send back to the owners of its halo nodes -- the appendix's extra
-    backward term.  It is not part of Eq. 6's constant-halo reading.
+    partition's rows send back to the owners of its halo nodes in the SAME iteration --
+    the exact (zero-staleness) variant of the appendix's term; the paper's own term uses
+    the previous iteration's D~^(t-1) (oracle_train halo_grad='prev_epoch').  It
+    is not part of Eq. 6's constant-halo reading.
     """
     P = prop_matrix(part)
     D = np.asarray(g_out, dtype=np.float64)

@@ -27,7 +27,8 @@ import numpy as np
 import scipy.sparse as sp
 
 from .partition import oracle_partition
-from .gcn import layer_forward, layer_backward, cross_entropy, sgd_step, adam_step, normalize_rows
+from .gcn import (layer_forward, layer_backward, cross_entropy, sgd_step, adam_step,
+                  normalize_rows, prop_matrix)
 
 
 def bf16_round(x):
@@ -91,6 +92,8 @@ class EpochRecord:
     reps: dict = field(default_factory=dict)            # l -> global [N, d_l] DIGEST H^(l)
     part_out: dict = field(default_factory=dict)        # (l, m) -> dict(A,Z,H)
     eps: dict = field(default_factory=dict)             # l -> max_u ||h~_u - h_u||
+    part_d: dict = field(default_factory=dict)          # (l, m) -> D^(l) of the part
+    halo_grad_sent: dict = field(default_factory=dict)  # (l, m) -> G_halo rows returned
 
 
 @dataclass
@@ -107,10 +110,16 @@ def oracle_train(indptr, indices, x, y, train_mask, weights, num_classes, part_o
                  cold_start="zero", mode="stale", normalize_pushed=False,
                  loss_weighting="count", record_outputs=False, parts=None,
                  halo_grad="none", store_dtype="fp32") -> OracleRun:
-    """halo_grad: 'none' (halo inputs are constants, P:810 -- the default) or
-    'same_epoch' (the appendix's P_out^T D W^T term, computed by each
-    part for its halo rows and returned to the owners in the same iteration)."""
-    if halo_grad not in ("none", "same_epoch"):
+    """halo_grad (the gradient a part sends back for its halo rows):
+      'none'        halo inputs are constants of the iteration (P:810, Eq. 6) -- default;
+      'prev_epoch'  the appendix's DIGEST backward, literally:
+                    G~_H^(t) = P_in^T D~^(t) (W~^(t))^T + P_out^T D~^(t-1) (W~^(t))^T, i.e.
+                    each part keeps S^(t) = P_out^T D~^(t) of its halo rows and, in
+                    iteration t+1, returns S^(t) (W^(t+1))^T to the owners (zero at t=1);
+      'same_epoch'  the exact (zero-staleness) variant: P_out^T D~^(t) (W^(t))^T returned in
+                    the same iteration t -- with fresh halos every G_W equals full-graph GCN
+                    (reading A16).  Not the paper's term; the exact reference for it."""
+    if halo_grad not in ("none", "same_epoch", "prev_epoch"):
         raise ValueError(halo_grad)
     if store_dtype not in ("fp32", "bf16"):
         raise ValueError(store_dtype)
@@ -147,6 +156,9 @@ def oracle_train(indptr, indices, x, y, train_mask, weights, num_classes, part_o
     halo = {(l, m): committed[l][p.halo_ids].copy() for l in range(1, L) for m, p in enumerate(parts)}
     halo_ver = {(l, m): version[l][p.halo_ids].copy() for l in range(1, L) for m, p in enumerate(parts)}
     opt_state = [(np.zeros_like(w), np.zeros_like(w)) for w in W]
+    # prev_epoch: S^(t-1) = P_out^T D~^(t-1) per (layer l >= 2, part m), zero before t = 1
+    s_prev = {(l, m): np.zeros((p.n_halo, dims[l])) for l in range(2, L + 1)
+              for m, p in enumerate(parts)}
 
     run = OracleRun(parts, [], W)
     for r in range(1, epochs + 1):
@@ -206,10 +218,19 @@ def oracle_train(indptr, indices, x, y, train_mask, weights, num_classes, part_o
                                    need_g_halo=(halo_grad == "same_epoch" and l >= 2))
                 total[l - 1] += b["G_W"]
                 gin[m], ghalo[m] = b["G_in"], b["G_halo"]
-            if l >= 2 and halo_grad == "same_epoch":
-                # P:816 term, returned in the same iteration: rows of G_halo of part m go to
-                # the owners of its halo nodes and add into their G^(l-1) before sigma'
+                if record_outputs:
+                    rec.part_d[(l, m)] = b["D"]
+                if halo_grad == "prev_epoch" and l >= 2:
+                    # P_out^T D~^(t-1) (W~^(t))^T -- last iteration's D, this one's W
+                    P_out = prop_matrix(p)[:, p.n_local:]
+                    ghalo[m] = s_prev[(l, m)] @ W[l - 1].T
+                    s_prev[(l, m)] = P_out.T @ b["D"]
+            if l >= 2 and halo_grad != "none":
+                # the returned term: rows of G_halo of part m go to the owners of its halo
+                # nodes and add into their G^(l-1) before sigma'
                 for m, p in enumerate(parts):
+                    if record_outputs:
+                        rec.halo_grad_sent[(l, m)] = ghalo[m].copy()
                     owner = np.asarray(part_of)[p.halo_ids]
                     for k, pk in enumerate(parts):
                         sel = np.flatnonzero(owner == k)

@@ -1,4 +1,6 @@
-"""Pins for the oracle's halo-gradient return (the appendix term)."""
+"""Pins for the oracle's same-iteration halo-gradient return (halo_grad='same_epoch', the
+exact variant of the appendix term; the literal stale term P:816 is pinned in
+tests/test_oracle_pins.py)."""
 import numpy as np
 import pytest
 

@@ -1,0 +1,27 @@
+#!/bin/bash
+# Named steps for one GPU call:  gpurun -- 'bash tools/gpurun/run.sh STEP [STEP...]'
+# Every step writes gpurun_out/<tag>_<step>.log (TAG env, default "g").
+export PYTHONUNBUFFERED=1
+mkdir -p gpurun_out
+TAG=${TAG:-g}
+O=gpurun_out/${TAG}
+NCU=/usr/local/cuda/bin/ncu
+nvidia-smi --query-gpu=name,uuid,clocks.sm,clocks.max.sm,power.draw --format=csv > ${O}_smi.txt 2>&1
+for step in "$@"; do
+  case "$step" in
+    build)  python -m paper_2206_00057_b200.build > ${O}_build.log 2>&1 ;;
+    roof)   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -o tools/gather_roof tools/gather_roof.cu \
+              && timeout 900 tools/gather_roof > ${O}_roof.jsonl 2> ${O}_roof.err ;;
+    spmm)   timeout 900 python tools/spmm_bench.py --widths 256,100,48 > ${O}_spmm.log 2>&1 ;;
+    spmm8)  timeout 900 python tools/spmm_bench.py --parts 8 --widths 256,100,48 > ${O}_spmm8.log 2>&1 ;;
+    async)  timeout 900 python -m pytest tests/test_gpu_async.py -q -x -p no:cacheprovider > ${O}_async.log 2>&1 ;;
+    tests)  timeout 3000 python -m pytest tests -q -m gpu -p no:cacheprovider > ${O}_tests.log 2>&1; echo "rc=$?" >> ${O}_tests.log ;;
+    fast)   timeout 2400 python -m pytest tests -q -m "gpu and not slow" -p no:cacheprovider > ${O}_fast.log 2>&1; echo "rc=$?" >> ${O}_fast.log ;;
+    smoke)  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > ${O}_smoke.log 2>&1; echo "rc=$?" >> ${O}_smoke.log ;;
+    bench)  timeout 900 python bench.py > ${O}_bench.log 2>&1 ;;
+    launches) timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none --csv \
+              --log-file ${O}_launches.csv python bench.py --steps 2 --warmup 1 --no-e2e > ${O}_launches.log 2>&1 ;;
+    *)      echo "unknown step $step" >> ${O}_errors.log ;;
+  esac
+done
+ls -la gpurun_out > ${O}_ls.txt

@@ -274,7 +274,7 @@ digest_status digest_layer_mask(const digest_part* part, int32_t d_in, int32_t d
  * n_local x d_in tensor (ld_gm floats; factor 1[gin_mask > 0], e.g. the previous H)
  * or, with flags DIGEST_BWD_GIN_MASK_BITS, a 1-bit mask (ld_gm 32-bit words per row,
  * e.g. digest_layer_mask of the previous layer). */
-enum { DIGEST_BWD_G_IS_D = 1u, DIGEST_BWD_GIN_MASK_BITS = 2u };
+enum { DIGEST_BWD_G_IS_D = 1u, DIGEST_BWD_GIN_MASK_BITS = 2u, DIGEST_BWD_HALO_SAVE_S = 4u };
 digest_status digest_layer_bwd(const digest_part* part, const float* X_local, int64_t ld_x,
                                const float* X_halo, int64_t ld_xh, const float* W,
                                int32_t d_in, int32_t d_out, int32_t act, int32_t order,
@@ -284,7 +284,13 @@ digest_status digest_layer_bwd(const digest_part* part, const float* X_local, in
                                int64_t ld_gm, float* G_halo, int64_t ld_gh, void* scratch,
                                void* stream);
 /* G_halo (n_halo x d_in, ld_gh; NULL = skip) = P_out^T D W^T: the gradient of this
- * part's halo rows, unmasked, for digest_return_halo_grad. */
+ * part's halo rows, unmasked, for digest_return_halo_grad, returned in the SAME
+ * iteration (the exact / zero-staleness variant of the appendix term).
+ * With flags DIGEST_BWD_HALO_SAVE_S, G_halo (n_halo x d_out, ld_gh >= d_out) instead
+ * receives S = P_out^T D~^(t), the part of the term the paper's DIGEST backward returns
+ * ONE iteration later (G~_H^(t) = P_in^T D~^(t) W~^(t)T + P_out^T D~^(t-1)
+ * W~^(t)T); the caller keeps it and forms next iteration's rows with
+ * digest_gemm(S, W, G, DIGEST_GEMM_BT) = S W^T at the then-current W. */
 
 /* The propagation product alone (the aggregation of Eq. 5 / its transposes):
  *   mode 0: Y = P_m X_ext      (n_local rows; X_ext = [X_local ; X_halo], width w)
@@ -361,7 +367,10 @@ digest_status digest_adam_step_dev(float* W, const float* G, float* m, float* v,
 
 /* ------------------------------------------------------------------ dense helper
  * C[M x N] = op(A[M x K] B[K x N]) in fp32 on the path the layer uses (exposed for
- * tests and the GEMM roofline).  flags bit0: ReLU epilogue. */
+ * tests, the GEMM roofline and the stale halo-gradient term).  flags bit0
+ * (DIGEST_GEMM_RELU): ReLU epilogue; bit1 (DIGEST_GEMM_BT): B is given transposed, as
+ * an N x K row-major matrix (ldb >= K), so C = A B^T -- e.g. S W^T with W d_in x d_out. */
+enum { DIGEST_GEMM_RELU = 1u, DIGEST_GEMM_BT = 2u };
 digest_status digest_gemm(const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
                           int64_t ldc, int64_t M, int32_t N, int32_t K, uint32_t flags,
                           void* stream);

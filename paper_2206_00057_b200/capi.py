@@ -327,6 +327,9 @@ def digest_layer_mask(part, d_in, d_out, order, saved):
 
 BWD_G_IS_D = 1
 BWD_GIN_MASK_BITS = 2
+BWD_HALO_SAVE_S = 4
+GEMM_RELU = 1
+GEMM_BT = 2
 
 
 def digest_layer_bwd(part, X_local, X_halo, ld_xh, W, d_in, d_out, act, order, saved, H_out,
@@ -399,11 +402,16 @@ def digest_adam_step(W, G, m, v, lr, b1, b2, eps, step, stream=None):
                                 stream_ptr(stream)))
 
 
-def digest_gemm(A, B, Cm, relu=False, stream=None):
-    M, K = A.shape
-    N = B.shape[1]
-    _check(lib.digest_gemm(ptr(A), ld_of(A), ptr(B), ld_of(B), ptr(Cm), ld_of(Cm), M, N, K,
-                           1 if relu else 0, stream_ptr(stream)))
+def digest_gemm(A, B, Cm, relu=False, stream=None, bt=False, M=None, ldc=None):
+    """C = A B (bt: C = A B^T, B given N x K).  Cm may be a tensor or a raw device address
+    (then pass M rows and its ldc)."""
+    Mr, K = A.shape
+    M = Mr if M is None else M
+    N = B.shape[0] if bt else B.shape[1]
+    ldc = ld_of(Cm) if ldc is None else ldc
+    _check(lib.digest_gemm(ptr(A), ld_of(A), ptr(B), ld_of(B), ptr(Cm), ldc, M, N, K,
+                           (GEMM_RELU if relu else 0) | (GEMM_BT if bt else 0),
+                           stream_ptr(stream)))
 
 
 # ------------------------------------------------------------------ DIGEST-A parameter server

@@ -100,7 +100,7 @@ dg::SpmmArgs spmm_full(const digest_part* p, const float* X0, int64_t ld0, const
   a.ld0 = ld0;
   a.split = p->n_local;
   a.x0_rows = p->n_local;
-  a.X1 = X1;
+  a.X1 = p->n_halo > 0 ? X1 : nullptr;   // no halo columns: a single-source product
   a.ld1 = ld1;
   a.Y = Y;
   a.ldy = ldy;
@@ -252,7 +252,8 @@ digest_status digest_layer_bwd(const digest_part* p, const float* X_local, int64
            (long long)ld_gm, (d_in + 31) / 32);
   const float* gm_f = gm_bits ? nullptr : static_cast<const float*>(gin_mask);
   const uint32_t* gm_b = gm_bits ? static_cast<const uint32_t*>(gin_mask) : nullptr;
-  if (G_halo && pl.h > 0) DG_TRY(check_mat(G_halo, ld_gh, d_in, "G_halo"));
+  const bool save_s = (flags & DIGEST_BWD_HALO_SAVE_S) != 0;   // G_halo <- P_out^T D
+  if (G_halo && pl.h > 0) DG_TRY(check_mat(G_halo, ld_gh, save_s ? d_out : d_in, "G_halo"));
   const bool want_halo = G_halo && pl.h > 0;
   DG_ARG(W && G_W && scratch, DIGEST_E_INVALID, "W, G_W and scratch must be non-NULL");
   cudaStream_t s = dg::as_stream(stream);
@@ -283,7 +284,7 @@ digest_status digest_layer_bwd(const digest_part* p, const float* X_local, int64
     void* wsc = carve(scratch, off, 0);
     dg::WgradSeg seg{A, pl.ldi, D, ldd, nullptr, 0, pl.n};
     DG_TRY(dg::wgrad(&seg, 1, d_in, d_out, G_W, wsc, s));
-    if (G_in || want_halo) {
+    if (G_in || (want_halo && !save_s)) {
       // U = D W^T : B(k, j) = W[j, k]
       dg::GemmArgs g = gemm_rm(D, ldd, W, d_out, U, pl.ldi, pl.n, d_in, d_out, 0);
       g.sBk = 1;
@@ -298,7 +299,9 @@ digest_status digest_layer_bwd(const digest_part* p, const float* X_local, int64
       a.ldmb = ld_gm;
       DG_TRY(dg::spmm(a, s));
     }
-    if (want_halo)   // P:816 term for the owners of the halo rows: G_halo = P_out^T U
+    if (want_halo && save_s)   // S = P_out^T D~^(t), returned next iteration
+      DG_TRY(dg::spmm(spmm_rh(p, D, ldd, G_halo, ld_gh, d_out), s));
+    else if (want_halo)        // same-iteration return: G_halo = P_out^T U
       DG_TRY(dg::spmm(spmm_rh(p, U, pl.ldi, G_halo, ld_gh, d_in), s));
   } else {
     DG_TRY(check_mat(X_local, ld_x, d_in, "X_local"));
@@ -306,10 +309,13 @@ digest_status digest_layer_bwd(const digest_part* p, const float* X_local, int64
     float* S = carve(scratch, off, sizeof(float) * (pl.n + pl.h) * pl.ldo);
     void* wsc = carve(scratch, off, 0);
     DG_TRY(dg::spmm(spmm_in(p, D, ldd, S, pl.ldo, d_out), s));
-    if (pl.h > 0)   // S_halo = P_out^T D (reverse-halo CSR, no atomics)
-      DG_TRY(dg::spmm(spmm_rh(p, D, ldd, S + pl.n * pl.ldo, pl.ldo, d_out), s));
+    // S_halo = P_out^T D (reverse-halo CSR, no atomics); with HALO_SAVE_S written
+    // straight into the caller's G_halo, which also feeds the weight gradient
+    float* Sh = want_halo && save_s ? G_halo : S + pl.n * pl.ldo;
+    const int64_t ldsh = want_halo && save_s ? ld_gh : pl.ldo;
+    if (pl.h > 0) DG_TRY(dg::spmm(spmm_rh(p, D, ldd, Sh, ldsh, d_out), s));
     dg::WgradSeg segs[2] = {{X_local, ld_x, S, pl.ldo, nullptr, 0, pl.n},
-                            {X_halo, ld_xh, S + pl.n * pl.ldo, pl.ldo, nullptr, 0, pl.h}};
+                            {X_halo, ld_xh, Sh, ldsh, nullptr, 0, pl.h}};
     DG_TRY(dg::wgrad(segs, pl.h > 0 ? 2 : 1, d_in, d_out, G_W, wsc, s));
     if (G_in) {
       dg::GemmArgs g = gemm_rm(S, pl.ldo, W, d_out, G_in, ld_gi, pl.n, d_in, d_out, 0);
@@ -321,7 +327,7 @@ digest_status digest_layer_bwd(const digest_part* p, const float* X_local, int64
       g.ldmb = ld_gm;
       DG_TRY(dg::gemm(g, s));
     }
-    if (want_halo) {   // P:816 term for the owners of the halo rows: G_halo = S_halo W^T
+    if (want_halo && !save_s) {   // same-iteration return: G_halo = S_halo W^T
       dg::GemmArgs g = gemm_rm(S + pl.n * pl.ldo, pl.ldo, W, d_out, G_halo, ld_gh, pl.h, d_in,
                                d_out, 0);
       g.sBk = 1;
@@ -351,10 +357,15 @@ digest_status digest_gemm(const float* A, int64_t lda, const float* B, int64_t l
                           int64_t ldc, int64_t M, int32_t N, int32_t K, uint32_t flags,
                           void* stream) {
   DG_ARG(A && B && C, DIGEST_E_INVALID, "NULL matrix");
-  DG_ARG(M >= 0 && N > 0 && K > 0 && lda >= K && ldb >= N && ldc >= N, DIGEST_E_SHAPE,
-         "bad GEMM shape");
-  return dg::gemm(gemm_rm(A, lda, B, ldb, C, ldc, M, N, K, (int)(flags & 1u)),
-                  dg::as_stream(stream));
+  const bool bt = (flags & DIGEST_GEMM_BT) != 0;
+  DG_ARG(M >= 0 && N > 0 && K > 0 && lda >= K && ldb >= (bt ? K : N) && ldc >= N,
+         DIGEST_E_SHAPE, "bad GEMM shape");
+  dg::GemmArgs g = gemm_rm(A, lda, B, ldb, C, ldc, M, N, K, (int)(flags & DIGEST_GEMM_RELU));
+  if (bt) {   // B(k, j) = B_given[j, k]
+    g.sBk = 1;
+    g.sBj = ldb;
+  }
+  return dg::gemm(g, dg::as_stream(stream));
 }
 
 }  // extern "C"

@@ -348,6 +348,101 @@ __global__ void __launch_bounds__(256, MB) k_spmm_rt(SpmmArgs a) {
   }
 }
 
+// Lean narrow-slab kernel (w <= 64 floats per launch; wider products run as column
+// slabs of it, see spmm_slab_width).  Same lane layout as k_spmm -- warp per row, EG =
+// 32/LC edge groups x LC lanes x VPL float4 -- but built for the instruction budget of an
+// L2-fabric-bound gather (tools/gather_roof.cu: ~18-20 TB/s of L2-resident row gathers on
+// this B200): 32-bit source offsets (one IMAD.WIDE.U32 per gather: the hot bit 31 is
+// shifted out and the row stride halved), one base select for two-source products (X1 is
+// pre-offset by -split rows, so both sources index with the same column), no per-gather
+// predicate selects (lanes past the chunk read vals of 0 and skip the load), the next
+// chunk's (col, val) prefetched under the current gathers, and a warp-uniform exit from
+// the unrolled steps of a short chunk.  RAG: the slab is not a multiple of 4*LC floats
+// (the last float4 of a lane is predicated on the slab width).
+template <int LC, int VPL, int UNR, bool TWO, bool RAG, int MB>
+__global__ void __launch_bounds__(256, MB) k_spmm_n(SpmmArgs a, const char* __restrict__ x0,
+                                                    const char* __restrict__ x1m,
+                                                    uint32_t split, uint32_t rb_half) {
+  constexpr int EG = 32 / LC;
+  constexpr int STEP = EG * UNR;
+  constexpr int STEPS = (32 + STEP - 1) / STEP;
+  const int lane = threadIdx.x & 31;
+  const int cl = lane % LC;
+  const int g = lane / LC;
+  const int w4 = a.width >> 2;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t row = warp; row < a.n_rows; row += nwarps) {
+    float4 acc[VPL];
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int64_t beg = a.row_ptr[row];
+    const int64_t end = a.in_len ? beg + a.in_len[row] : a.row_ptr[row + 1];
+    int32_t c_nxt = 0;
+    float v_nxt = 0.f;
+    if (beg + lane < end) {
+      c_nxt = __ldg(a.col + beg + lane);
+      v_nxt = __ldg(a.val + beg + lane);
+    }
+    for (int64_t e0 = beg; e0 < end; e0 += 32) {
+      const int32_t c = c_nxt;
+      const float v = v_nxt;
+      const int cnt = (int)min((int64_t)32, end - e0);
+      c_nxt = 0;
+      v_nxt = 0.f;
+      if (e0 + 32 + lane < end) {
+        c_nxt = __ldg(a.col + e0 + 32 + lane);
+        v_nxt = __ldg(a.val + e0 + 32 + lane);
+      }
+#pragma unroll
+      for (int st = 0; st < STEPS; ++st) {
+        if (st * STEP >= cnt) break;   // warp-uniform
+        // Lanes past the chunk hold (col 0, val 0): their gathers read source row 0
+        // (valid, L1-resident) and contribute 0 -- no predicates, so every load of the
+        // step issues before the first FMA waits.  RAG: the last float4 of a lane past
+        // the slab re-reads the slab's last float4 into an accumulator never stored.
+        float4 t[UNR][VPL];
+        float x[UNR];
+        const float4* p[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          const int j = st * STEP + u * EG + g;
+          const uint32_t cr = (uint32_t)__shfl_sync(0xffffffffu, c, j);
+          x[u] = __shfl_sync(0xffffffffu, v, j);
+          const char* base = x0;
+          if (TWO) base = (cr & 0x7fffffffu) >= split ? x1m : x0;
+          p[u] = reinterpret_cast<const float4*>(base + (uint64_t)(cr << 1) * rb_half);
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+#pragma unroll
+          for (int q = 0; q < VPL; ++q) {
+            const int idx = cl + q * LC;
+            t[u][q] = __ldg(p[u] + (RAG && q == VPL - 1 ? min(idx, w4 - 1) : idx));
+          }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+#pragma unroll
+          for (int q = 0; q < VPL; ++q) {
+            acc[q].x = fmaf(x[u], t[u][q].x, acc[q].x);
+            acc[q].y = fmaf(x[u], t[u][q].y, acc[q].y);
+            acc[q].z = fmaf(x[u], t[u][q].z, acc[q].z);
+            acc[q].w = fmaf(x[u], t[u][q].w, acc[q].w);
+          }
+      }
+    }
+#pragma unroll
+    for (int off = LC; off < 32; off <<= 1)   // tree over the edge groups
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) {
+        acc[q].x += __shfl_down_sync(0xffffffffu, acc[q].x, off);
+        acc[q].y += __shfl_down_sync(0xffffffffu, acc[q].y, off);
+        acc[q].z += __shfl_down_sync(0xffffffffu, acc[q].z, off);
+        acc[q].w += __shfl_down_sync(0xffffffffu, acc[q].w, off);
+      }
+    spmm_row_epilogue<LC, VPL>(a, row, lane, cl, g, w4, acc);
+  }
+}
 
 // Single-source product through TMA row gathers (tile::gather4), experimental
 // (DIGEST_SPMM_TMA=1; measured 1.45-1.6x SLOWER than the load-based kernels at w=48/100,
@@ -642,6 +737,82 @@ digest_status launch(const SpmmArgs& a, cudaStream_t s) {
   return DIGEST_OK;
 }
 
+// Lean narrow-slab kernel launch (w4 = width/4 in 5..16).  Byte/flop accounting as in
+// launch(): the slab's share of the whole product's edge-gather bytes.
+template <int LC, int VPL, int UNR, bool RAG, int MB>
+digest_status launch_n(const SpmmArgs& a, cudaStream_t s) {
+  const double W = a.full_width > 0 ? a.full_width : a.width;
+  const double frac = a.width / W;
+  const double bytes = frac * ((double)a.nnz * (8.0 + 4.0 * W) + (double)a.n_rows * (4.0 * W + 8.0));
+  const double flops = 2.0 * (double)a.nnz * a.width;
+  const bool two = !(a.in_len != nullptr || a.X1 == nullptr || a.split >= INT32_MAX);
+  const char* x0 = reinterpret_cast<const char*>(a.X0);
+  const char* x1m = two ? reinterpret_cast<const char*>(a.X1) - a.split * a.ld1 * 4 : x0;
+  const uint32_t rb_half = (uint32_t)(a.ld0 * 2);
+  int64_t blocks = ceil_div(a.n_rows, 8);
+  if (two) {
+    static const int64_t cap = resident_ctas(k_spmm_n<LC, VPL, UNR, true, RAG, MB>);
+    if (blocks > cap) blocks = cap;
+    DG_LAUNCH_TAG(DIGEST_PROF_SPMM, (int)W, s, bytes, flops, (k_spmm_n<LC, VPL, UNR, true, RAG, MB>),
+                  (unsigned)blocks, 256, 0, a, x0, x1m, (uint32_t)a.split, rb_half);
+  } else {
+    static const int64_t cap = resident_ctas(k_spmm_n<LC, VPL, UNR, false, RAG, MB>);
+    if (blocks > cap) blocks = cap;
+    DG_LAUNCH_TAG(DIGEST_PROF_SPMM, (int)W, s, bytes, flops, (k_spmm_n<LC, VPL, UNR, false, RAG, MB>),
+                  (unsigned)blocks, 256, 0, a, x0, x1m, (uint32_t)INT32_MAX, rb_half);
+  }
+  return DIGEST_OK;
+}
+
+// The lean kernel applies when the two sources share one row stride and every offset
+// fits 32 bits (source rows < 2^31, row bytes < 2^32).
+bool narrow_ok(const SpmmArgs& a) {
+  const int w4 = a.width / 4;
+  if (w4 < 5 || w4 > 16) return false;
+  const bool two = !(a.in_len != nullptr || a.X1 == nullptr || a.split >= INT32_MAX);
+  if (two && a.ld1 != a.ld0) return false;
+  return a.ld0 > 0 && a.ld0 * 2 < (int64_t)UINT32_MAX;
+}
+
+// DIGEST_SPMM_N (experiment switch): 0 = the round-1 kernels for narrow widths; 1..
+// variants of the lean kernel (default 1).
+int narrow_variant() {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = dg::knob("DIGEST_SPMM_N");
+    v = e ? atoi(e) : 1;
+  }
+  return v;
+}
+
+digest_status launch_narrow(const SpmmArgs& a, cudaStream_t s) {
+  const int w4 = a.width / 4;
+  const int v = narrow_variant();
+  if (w4 == 12) {
+    switch (v) {
+      case 2: return launch_n<4, 3, 4, false, 4>(a, s);
+      case 3: return launch_n<4, 3, 2, false, 1>(a, s);
+      case 4: return launch_n<4, 3, 1, false, 4>(a, s);
+      default: return launch_n<4, 3, 2, false, 4>(a, s);
+    }
+  }
+  if (w4 == 16) {
+    switch (v) {
+      case 2: return launch_n<4, 4, 4, false, 4>(a, s);
+      case 3: return launch_n<8, 2, 4, false, 4>(a, s);
+      case 4: return launch_n<4, 4, 1, false, 4>(a, s);
+      default: return launch_n<4, 4, 2, false, 4>(a, s);
+    }
+  }
+  if (w4 == 8) {
+    if (v == 3) return launch_n<8, 1, 4, false, 4>(a, s);
+    return launch_n<4, 2, 2, false, 4>(a, s);
+  }
+  if (w4 <= 7) return launch_n<4, 2, 2, true, 4>(a, s);
+  if (w4 <= 11) return launch_n<4, 3, 2, true, 4>(a, s);
+  return launch_n<4, 4, 2, true, 4>(a, s);
+}
+
 }  // namespace
 
 digest_status spmm_one(const SpmmArgs& a, cudaStream_t s);
@@ -650,14 +821,23 @@ digest_status spmm_one(const SpmmArgs& a, cudaStream_t s);
 // sized to stay resident in L2 while the row window sweeps a graph block, so the
 // edge gathers hit L2 instead of HBM; each slab re-reads the CSR (8 B / nnz).
 // DIGEST_SPMM_SLAB overrides the slab width (0 = no slabs).
+// Otherwise (auto) widths above `smax` floats are cut into balanced slabs of at most
+// smax (a multiple of 32 when 1-bit masks are read or written, so mask words stay whole)
+// that the lean narrow kernel runs; DIGEST_SPMM_SMAX overrides smax (0 = no slabs).
 int spmm_slab_width(const SpmmArgs& a) {
-  static int env = -2;
+  static int env = -2, smax = -2;
   if (env == -2) {
     const char* e = dg::knob("DIGEST_SPMM_SLAB");
     env = e ? atoi(e) : -1;
+    const char* m = dg::knob("DIGEST_SPMM_SMAX");
+    smax = m ? atoi(m) : 0;
   }
   if (env >= 0) return env;
-  return 0;
+  if (smax <= 0 || narrow_variant() == 0 || a.width <= smax) return 0;
+  const int nslab = (a.width + smax - 1) / smax;
+  int slab = (int)round_up(ceil_div(a.width, nslab), 4);
+  if (a.mbits || a.obits || a.mask) slab = (int)round_up(slab, 32);
+  return slab;
 }
 
 digest_status spmm(const SpmmArgs& a0, cudaStream_t s) {
@@ -702,6 +882,7 @@ digest_status spmm(const SpmmArgs& a0, cudaStream_t s) {
 
 digest_status spmm_one(const SpmmArgs& a, cudaStream_t s) {
   const int w4 = a.width / 4;
+  if (narrow_variant() > 0 && narrow_ok(a)) return launch_narrow(a, s);
   static int tg = -1;   // DIGEST_SPMM_TMA=1: TMA row-gather kernel for single-source products
   if (tg < 0) {
     const char* e = dg::knob("DIGEST_SPMM_TMA");

@@ -36,11 +36,22 @@ class TrainConfig:
     pull_mode: int = D.PULL_FLIP
     fresh: bool = False         # zero-staleness mode (the oracle's mode='fresh')
     cache_l1: bool = False      # aggregate the static layer-1 inputs once
-    halo_grad: bool = False     # return P_out^T D W^T to the halo owners
+    # SURVEY f2, the gradient returned to the owners of a part's halo rows:
+    #   '' / False / 'none'   halo inputs are constants (Eq. 6; default)
+    #   'prev_epoch'          the paper's DIGEST backward: P_out^T D~^(t-1) W~^(t)T
+    #   'same_epoch' / True   the exact variant: P_out^T D~^(t) W~^(t)T in the same iteration
+    halo_grad: object = 
     transport: str = "nccl"     # multi-process exchange: 'nccl' or 'peer' (CUDA IPC windows)
     async_store: bool = False   # DIGEST-A on the peer transport: NOWAIT pushes, SNAPSHOT pulls
     store_bf16: bool = False    # bf16 stale store / transfers
     device_step: bool = False   # Adam step count on the device (CUDA-graph capturable epochs)
+
+    def __post_init__(self):
+        hg = self.halo_grad
+        hg = "same_epoch" if hg is True else ("" if hg in (False, None, "none") else hg)
+        if hg not in ("", "same_epoch", "prev_epoch"):
+            raise ValueError(f"halo_grad {self.halo_grad!r}")
+        self.halo_grad = hg
 
 
 class Partition:
@@ -129,6 +140,10 @@ class DigestWorker:
             from .dist import connect_peer_store
             connect_peer_store(self.store, part.num_parts)   # collective over the process group
         self.pulls = self.pushes = 0
+        # halo_grad='prev_epoch': S^(t-1) = P_out^T D~^(t-1) per layer l >= 2 (zero at t = 1)
+        self.s_prev = {}
+        if cfg.halo_grad == "prev_epoch" and h > 0:
+            self.s_prev = {l: torch.zeros(h, dims[l], device=dev) for l in range(2, self.L + 1)}
 
     # --------------------------------------------------------------- schedule pieces
     def halo_input(self, l):
@@ -196,16 +211,23 @@ class DigestWorker:
         xl = self.x_local if l == 1 else self.H[l - 1]
         xh, ldh = self.halo_input(l)
         act = D.ACT_RELU if l < self.L else D.ACT_NONE
-        gh, ldgh = None, 0
+        gh, ldgh, hflags = None, 0, 0
         if self.cfg.halo_grad and l >= 2 and self.part.n_halo > 0:
             gh, ldgh = D.digest_store_grad_buffer(self.store, l - 1)
+            if self.cfg.halo_grad == "prev_epoch":
+                # the rows returned now are S^(t-1) W^(t)T; this backward then
+                # overwrites S with S^(t) = P_out^T D~^(t) (stream order: read, then write)
+                S = self.s_prev[l]
+                D.digest_gemm(S, self.W[l - 1], gh, bt=True, M=self.part.n_halo, ldc=ldgh,
+                              stream=stream)
+                gh, ldgh, hflags = S, 0, D.BWD_HALO_SAVE_S
         # G_in of layer l is produced already multiplied by 1[H^(l-1) > 0] (the 1-bit
         # mask of layer l-1), i.e. it is D^(l-1); layer l-1 then skips its own masking
         # pass (DIGEST_BWD_G_IS_D).
         D.digest_layer_bwd(self.part.handle, xl, xh, ldh, self.W[l - 1], dims[l - 1], dims[l],
                            act, self.layer_order(l), self.saved[l], None, self.G[l],
                            self.GW[l - 1], self.G[l - 1] if l >= 2 else None, self.scratch,
-                           stream, flags=D.BWD_G_IS_D if l < self.L else 0,
+                           stream, flags=(D.BWD_G_IS_D if l < self.L else 0) | hflags,
                            gin_mask=self.mask_bits[l - 1] if l >= 2 else None, G_halo=gh,
                            ld_gh=ldgh)
 

@@ -1,4 +1,6 @@
-"""GPU path vs oracle for the halo-gradient return (the P:816 term)."""
+"""GPU path vs oracle for the halo-gradient return: the paper's stale term
+P_out^T D~^(t-1) W~^(t)T (halo_grad='prev_epoch') and its exact same-iteration
+variant (halo_grad='same_epoch')."""
 import numpy as np
 import pytest
 import torch
@@ -84,4 +86,79 @@ def test_trajectory_with_halo_grad(M, fresh, N):
                 assert rel(ws[0].GW[l].cpu().numpy(), gref) <= TOL, l
     for l, wref in enumerate(run.weights):
         assert rel(ws[0].W[l].cpu().numpy(), wref) <= TOL
+    grp.close()
+
+
+@pytest.mark.parametrize("d_in,d_out,order", [(24, 40, 1), (40, 24, 2), (256, 48, 0),
+                                              (100, 256, 0)])
+def test_saved_s_per_call(d_in, d_out, order):
+    """DIGEST_BWD_HALO_SAVE_S: G_halo receives S = P_out^T D (width d_out) and G_W is
+    unchanged; S W^T through digest_gemm(bt) is the oracle's G_halo."""
+    Dm = D()
+    cfg = small_config(num_nodes=900, nnz=9000, d0=d_in, hidden=(d_out,), seed=15 + d_in)
+    ip, ix = make_graph(cfg)
+    part = make_random_parts(cfg.num_nodes, 3, 2)
+    p, _ = gpu_partition(ip, ix, part, 3, 1)
+    op = oracle.oracle_partition(ip, ix, part, 3, 1)
+    g = torch.Generator().manual_seed(3 * d_in + d_out)
+    xl = torch.rand(p.n_local, d_in, generator=g) * 2 - 1
+    xh = torch.rand(p.n_halo, d_in, generator=g) * 2 - 1
+    w = (torch.rand(d_in, d_out, generator=g) * 2 - 1) / np.sqrt(d_in)
+    gout = torch.randn(p.n_local, d_out, generator=g)
+    sv, sc = Dm.digest_layer_workspace(p.handle, d_in, d_out, order)
+    saved = torch.empty(max(sv, 256), dtype=torch.uint8, device="cuda")
+    scratch = torch.empty(max(sc, 256), dtype=torch.uint8, device="cuda")
+    H = torch.empty(p.n_local, d_out, device="cuda")
+    Dm.digest_layer_fwd(p.handle, xl.cuda(), xh.cuda(), d_in, w.cuda(), d_in, d_out, 1, order, H,
+                        saved, scratch)
+    GW = torch.empty(d_in, d_out, device="cuda")
+    Gin = torch.empty(p.n_local, d_in, device="cuda")
+    S = torch.full((p.n_halo, d_out), 9.0, device="cuda")
+    Dm.digest_layer_bwd(p.handle, xl.cuda(), xh.cuda(), d_in, w.cuda(), d_in, d_out, 1, order,
+                        saved, H, gout.cuda(), GW, Gin, scratch, G_halo=S,
+                        flags=Dm.BWD_HALO_SAVE_S)
+    Gh = torch.empty(p.n_halo, d_in, device="cuda")
+    Dm.digest_gemm(S, w.cuda(), Gh, bt=True)
+    torch.cuda.synchronize()
+    b = layer_backward(op, xl.numpy(), xh.numpy(), w.numpy(), gout.numpy(),
+                       H.cpu().numpy() > 0, True, need_g_halo=True)
+    P_out = oracle.gcn.prop_matrix(op)[:, op.n_local:]
+    assert rel(S.cpu().numpy(), P_out.T @ b["D"]) <= TOL
+    assert rel(Gh.cpu().numpy(), b["G_halo"]) <= TOL
+    assert rel(GW.cpu().numpy(), b["G_W"]) <= TOL
+    assert rel(Gin.cpu().numpy(), b["G_in"]) <= TOL
+    p.close()
+
+
+@pytest.mark.parametrize("M,N,opt", [(2, 1, "sgd"), (3, 1, "sgd"), (3, 2, "adam")])
+def test_trajectory_with_stale_halo_grad(M, N, opt):
+    """halo_grad='prev_epoch' (P:816 literal) vs the oracle, per epoch; the stale term
+    changes the trajectory (it is not the constant-halo run)."""
+    from paper_2206_00057_b200.engine import TrainConfig, build_workers, LoopbackGroup
+    cfg = small_config(num_nodes=1000, nnz=11000, d0=20, hidden=(32, 16), num_classes=6, c_pad=8,
+                       seed=80 + M, train_frac=0.5)
+    inp = make_inputs(cfg)
+    part = make_random_parts(cfg.num_nodes, M, 4)
+    lr = 0.05 if opt == "sgd" else 0.01
+    tc = TrainConfig(dims=cfg.dims, num_classes=cfg.num_classes, sync_interval=N, lr=lr,
+                     optimizer=opt, halo_grad="prev_epoch")
+    ws = build_workers(inp.indptr, inp.indices, inp.x, inp.y, inp.train_mask, inp.weights, part, M, tc)
+    grp = LoopbackGroup(ws)
+    R = 4
+    kw = dict(sync_interval=N, epochs=R, lr=lr, optimizer=opt)
+    run = oracle.oracle_train(inp.indptr, inp.indices, inp.x, inp.y, inp.train_mask, inp.weights,
+                              cfg.num_classes, part, M, halo_grad="prev_epoch", **kw)
+    base = oracle.oracle_train(inp.indptr, inp.indices, inp.x, inp.y, inp.train_mask, inp.weights,
+                               cfg.num_classes, part, M, **kw)
+    for r in range(1, R + 1):
+        grp.epoch(r)
+        torch.cuda.synchronize()
+        loss = sum(w.loss.item() for w in ws)
+        assert abs(loss - run.records[r - 1].loss) <= TOL * abs(run.records[r - 1].loss), r
+        for l, gref in enumerate(run.records[r - 1].grads):
+            assert rel(ws[0].GW[l].cpu().numpy(), gref) <= TOL, (r, l)
+    for l, wref in enumerate(run.weights):
+        assert rel(ws[0].W[l].cpu().numpy(), wref) <= TOL
+    # the returned term is real: the first layer's weights leave the constant-halo run
+    assert rel(run.weights[0], base.weights[0]) > 10 * TOL
     grp.close()

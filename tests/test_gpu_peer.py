@@ -59,6 +59,10 @@ CASES = {
     "M3_stale_halo_grad": dict(world=3, parts_seed=9, epochs=4, graph=dict(GRAPH, seed=26),
                                train=dict(sync_interval=2, lr=0.05, optimizer="sgd",
                                           halo_grad=True)),
+    # the paper's stale halo-gradient return (one iteration late)
+    "M3_stale_halo_grad_prev": dict(world=3, parts_seed=9, epochs=4, graph=dict(GRAPH, seed=29),
+                                    train=dict(sync_interval=1, lr=0.05, optimizer="sgd",
+                                               halo_grad="prev_epoch")),
     # bf16 store: oracle with store_dtype='bf16', tolerance of
     # tests/test_gpu_bf16_store.py; the bit-identity with the loopback run still holds
     "M3_N1_bf16_store": dict(world=3, parts_seed=3, epochs=4, graph=dict(GRAPH, seed=27),
@@ -107,7 +111,8 @@ def test_peer_transport_multiprocess(name, tmp_path):
                               cfg.num_classes, part, M, sync_interval=tr["sync_interval"],
                               epochs=spec["epochs"], lr=tr["lr"], optimizer=tr["optimizer"],
                               mode="fresh" if tr.get("fresh") else "stale",
-                              halo_grad="same_epoch" if tr.get("halo_grad") else "none",
+                              halo_grad=("prev_epoch" if tr.get("halo_grad") == "prev_epoch"
+                                         else "same_epoch" if tr.get("halo_grad") else "none"),
                               store_dtype="bf16" if tr.get("store_bf16") else "fp32",
                               normalize_pushed=bool(tr.get("normalize_pushed")))
     tol = 5e-4 if tr.get("store_bf16") else TOL

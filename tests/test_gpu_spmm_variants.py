@@ -17,8 +17,18 @@ from oracle.gcn import layer_forward
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
-CASES = [(48, {"DIGEST_SPMM_V12": str(v)}) for v in range(8)]
-CASES += [(48, {"DIGEST_SPMM_PFH": "1"}), (48, {"DIGEST_SPMM_GRID": "1"})]
+# round-1 kernels for narrow widths (DIGEST_SPMM_N=0 turns the lean kernel off)
+CASES = [(48, {"DIGEST_SPMM_V12": str(v), "DIGEST_SPMM_N": "0"}) for v in range(8)]
+CASES += [(48, {"DIGEST_SPMM_PFH": "1", "DIGEST_SPMM_N": "0"}),
+          (48, {"DIGEST_SPMM_GRID": "1", "DIGEST_SPMM_N": "0"})]
+# the lean narrow-slab kernel: every variant, ragged slabs, all three products
+CASES += [(w, {"DIGEST_SPMM_N": str(n)}) for w in (48, 64, 32) for n in (1, 2, 3, 4)]
+CASES += [(w, {"DIGEST_SPMM_N": "1", "MODE": m}) for w in (20, 36, 52, 48) for m in ("0", "1", "2")]
+# column slabs of the lean kernel (balanced, <= SMAX floats)
+CASES += [(w, {"DIGEST_SPMM_SMAX": sm, "MODE": m}) for w, sm in ((100, "64"), (100, "48"),
+                                                                  (256, "64"), (256, "32"),
+                                                                  (128, "64"), (1024, "64"))
+          for m in ("0", "1", "2")]
 CASES += [(100, {"DIGEST_SPMM_V25": str(v)}) for v in range(6)]
 CASES += [(256, {"DIGEST_SPMM_V": str(v)}) for v in range(7)]
 CASES += [(256, {"DIGEST_SPMM_SLAB": "64"}), (256, {"DIGEST_SPMM_HINTS": "0"}),
@@ -26,13 +36,14 @@ CASES += [(256, {"DIGEST_SPMM_SLAB": "64"}), (256, {"DIGEST_SPMM_HINTS": "0"}),
 CASES += [(w, {}) for w in (4, 8, 16, 32, 64, 128, 384, 512, 1024)]
 CASES += [(128, {"DIGEST_SPMM_V32": "1"})]
 # TMA row-gather kernel (single-source products): P_in (mode 1) and P_out^T (mode 2)
-CASES += [(w, {"DIGEST_SPMM_TMA": "1", "MODE": m}) for w in (4, 16, 48, 100, 128, 256)
-          for m in ("1", "2")]
-CASES += [(w, {"DIGEST_SPMM_MB": mb}) for w in (48, 100, 256) for mb in ("1", "4")]
+CASES += [(w, {"DIGEST_SPMM_TMA": "1", "DIGEST_SPMM_N": "0", "MODE": m})
+          for w in (4, 16, 48, 100, 128, 256) for m in ("1", "2")]
+CASES += [(w, {"DIGEST_SPMM_MB": mb, "DIGEST_SPMM_N": "0"}) for w in (48, 100, 256)
+          for mb in ("1", "4")]
 
 
 @pytest.mark.timeout(300)
-@pytest.mark.parametrize("width,env", CASES, ids=[f"w{w}-" + "-".join(f"{k[12:]}{v}" for k, v in e.items())
+@pytest.mark.parametrize("width,env", CASES, ids=[f"w{w}-" + "-".join(f"{k[-4:]}{v}" for k, v in e.items())
                                                   for w, e in CASES])
 def test_spmm_variant(width, env, tmp_path):
     if not torch.cuda.is_available():

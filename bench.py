@@ -14,10 +14,14 @@ Prints ONE JSON line on rank 0.
 tier) on the host cores, on a bounded sample of the same workload.
 """
 import argparse
+import csv
 import json
 import os
+import resource
+import socket
 import subprocess
 import sys
+import tempfile
 import threading
 import time
 
@@ -62,6 +66,8 @@ def parse():
                     help="bf16 stale store and transfers (SURVEY f3 (ii)); off by default")
     ap.add_argument("--cache-l1", action="store_true",
                     help="aggregate the static layer-1 inputs once (SURVEY f3 (i)); off by default")
+    ap.add_argument("--no-ncu", action="store_true",
+                    help="skip the ncu DRAM-traffic probe of the dominant kernel")
     return ap.parse_args()
 
 
@@ -140,18 +146,24 @@ def oracle_sample_epoch_seconds(cfg_name, M, frac, steps, warmup):
     inp = make_inputs(cfg)
     part = make_block_parts(cfg, M)
     parts = [oracle.oracle_partition(inp.indptr, inp.indices, part, M, m) for m in range(M)]
-    times = []
+    times, cpu = [], 0.0
     for i in range(warmup + steps):
+        r0 = resource.getrusage(resource.RUSAGE_SELF)
         t0 = time.perf_counter()
         oracle.oracle_train(inp.indptr, inp.indices, inp.x, inp.y, inp.train_mask, inp.weights,
                             cfg.num_classes, part, M, sync_interval=get_config(cfg_name).sync_interval,
                             epochs=1, parts=parts)
         if i >= warmup:
             times.append(time.perf_counter() - t0)
+            r1 = resource.getrusage(resource.RUSAGE_SELF)
+            cpu += (r1.ru_utime - r0.ru_utime) + (r1.ru_stime - r0.ru_stime)
     sample = (f"{steps} oracle epoch(s) of a {cfg_name}-shaped graph scaled to {frac:g} of the "
               f"nodes/edges ({cfg.num_nodes} nodes, {cfg.nnz} nnz, dims {list(cfg.dims)}, M={M}); "
               f"time x {1 / frac:g}")
-    return [t / frac for t in times], sample
+    # threads actually used: CPU seconds / wall seconds of the timed oracle epochs (SciPy's
+    # sparse products run on one thread, the dense products on the BLAS pool)
+    eff = cpu / max(sum(times), 1e-9)
+    return [t / frac for t in times], sample, round(eff, 2)
 
 
 def cores():
@@ -172,15 +184,16 @@ def reference_frac(a):
 def run_reference(a, rank, world):
     if rank != 0:
         return
-    per, sample = oracle_sample_epoch_seconds(a.config, world, reference_frac(a), a.steps,
-                                              a.warmup)
+    M = max(world, a.gpus)
+    per, sample, eff = oracle_sample_epoch_seconds(a.config, M, reference_frac(a), a.steps,
+                                                   a.warmup)
     v = float(np.mean(per))
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": a.config, "parts": world},
-            "cpu_baseline": {"value": v, "unit": "s", "cores": cores(), "kind": "oracle",
-                             "sample": sample},
+            "config": {"workload": a.config, "parts": M},
+            "cpu_baseline": {"value": v, "unit": "s", "cores": eff, "cores_available": cores(),
+                             "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -237,6 +250,16 @@ def run_ours(a, rank, world, local):
         ids = broadcast_ids(D.digest_comm_unique_id, 2, rank, device=coll_dev)
         comm_grad = D.digest_comm_init(ids[0], world, rank)
         comm_halo = D.digest_comm_init(ids[1], world, rank)
+    try:
+        uuid = str(torch.cuda.get_device_properties(torch.cuda.current_device()).uuid)
+    except Exception:   # noqa: BLE001
+        uuid = None
+    rank_info = {"rank": rank, "device": torch.cuda.current_device(), "uuid": uuid,
+                 "transport": a.transport if world > 1 else None,
+                 "exchange_init": "ok" if world == 1 or comm_grad is not None else "failed"}
+    print(f"bench rank {rank}/{world}: cuda:{rank_info['device']} {uuid} transport="
+          f"{rank_info['transport']} init={rank_info['exchange_init']}", file=sys.stderr,
+          flush=True)
 
     n_sync = a.sync_interval or cfg.sync_interval
     tc = TrainConfig(dims=cfg.dims, num_classes=cfg.num_classes, sync_interval=n_sync,
@@ -392,27 +415,49 @@ def run_ours(a, rank, world, local):
         e2e = {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": 8, "input_pipeline": "double-buffered, copy stream"}
 
-    # ---- roofline of the dominant kernel (the SpMM instantiation with the largest time)
+    # ---- roofline of the dominant kernel: the SpMM product (all its column-slab launches)
+    # of the width with the largest time.  HBM roof on the DRAM bytes ncu counts for one
+    # such product of this build (dram_probe, run below after the timed regions), the
+    # edge-gather model beside it, and the L2->SM gather roof measured on
+    # this B200 by tools/gather_roof.cu (profiles/r2_gather_roof.jsonl).
     hbm, bf16, src = peaks()
     dom = max((d for d in detail if d["cls"] == "spmm"), key=lambda d: d["ms"], default=None)
     roof = None
+    probe = None
+    if dom and dom["ms"] > 0 and rank == 0 and world == 1 and not loop and not a.no_ncu:
+        probe = dram_probe(a.config, M, rank, int(dom["tag"]))
     if dom and dom["ms"] > 0:
-        per_launch_bytes = dom["bytes"] / dom["launches"]
-        avg_s = dom["ms"] / 1e3 / dom["launches"]
-        ach = per_launch_bytes / avg_s / 1e9
-        roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-                "traffic": traffic_from_profiles(f"{a.config}_M{M}_spmm_w{dom['tag']}"),
-                "kernel": f"k_spmm width {dom['tag']}",
-                "peak_source": src, "launches": dom["launches"], "avg_ms": avg_s * 1e3,
-                "alg_bytes_per_launch": per_launch_bytes}
-        # The edge-gather bytes are served by L2 (hits) or HBM (misses), and every one of
-        # them passes the L2 slices, whose full-chip throughput is capped at ~6300 B per SM
-        # clock (B300_MICROARCH.md "LTS throughput cap", path-independent).  At the SM clock
-        # sampled during the timed region that cap is the roof this kernel actually meets.
-        if clocks.get("sm_mhz"):
-            lts = 6300.0 * clocks["sm_mhz"] * 1e6 / 1e9
-            roof["l2_slice_roof"] = {"peak": lts, "unit": "GB/s", "frac": ach / lts,
-                                     "basis": "6300 B/clk x median SM clock under load"}
+        W_ = int(dom["tag"])
+        rate_alg = dom["bytes"] / (dom["ms"] / 1e3)              # edge-gather B/s (all launches)
+        n_rows, n_src, nnz_ = info.n_local, info.n_local + info.n_halo, info.nnz
+        alg_prod = nnz_ * (8.0 + 4 * W_) + n_rows * (4.0 * W_ + 8)
+        compulsory = 8.0 * nnz_ + 4.0 * W_ * n_src + 4.0 * W_ * n_rows
+        n_prod = max(1, int(round(dom["bytes"] / alg_prod)))
+        avg_s = dom["ms"] / 1e3 / n_prod
+        roof = {"bound": "hbm", "unit": "GB/s", "peak": hbm, "peak_source": src,
+                "kernel": f"SpMM product width {W_} ({dom['launches'] // n_prod} launch(es) each)",
+                "products": n_prod, "avg_ms": avg_s * 1e3,
+                "alg_bytes_per_launch": alg_prod, "compulsory_bytes": compulsory}
+        if probe and probe.get("traffic"):
+            t = probe["traffic"]
+            roof.update({"achieved": t / avg_s / 1e9, "frac": t / avg_s / 1e9 / hbm,
+                         "traffic": t, "traffic_over_compulsory": t / compulsory,
+                         "achieved_basis": "ncu DRAM bytes (read+write) of one product in this "
+                                           "run / live mean product time (CUDA events)",
+                         "traffic_probe": probe})
+        else:
+            roof.update({"achieved": rate_alg / 1e9, "frac": rate_alg / 1e9 / hbm, "traffic": None,
+                         "achieved_basis": "edge-gather model (DRAM traffic unavailable: "
+                                           f"{(probe or {}).get('error', 'probe not run')})"})
+        roof["effective"] = {"achieved": rate_alg / 1e9, "frac": rate_alg / 1e9 / hbm,
+                             "model": "edge-gather bytes 8+4w per nonzero + 4w+8 per row "
+                                      "(SURVEY 8.d.4), every gathered row counted"}
+        l2 = gather_roof(W_)
+        if l2:
+            roof["l2_fabric"] = {"peak": l2["gbs"], "achieved": rate_alg / 1e9,
+                                 "frac": rate_alg / 1e9 / l2["gbs"],
+                                 "basis": f"L2-resident random row gathers, width {l2['width']} "
+                                          f"({l2['variant']}), profiles/r2_gather_roof.jsonl"}
     spmm = prof["spmm"]
     nnz_per_s = None
     gteps = None
@@ -420,11 +465,22 @@ def run_ours(a, rank, world, local):
         # nonzeros traversed = flops / (2 * width), summed per launch in the detail table
         nz = sum(d["flops"] / (2.0 * d["tag"]) for d in detail if d["cls"] == "spmm" and d["tag"])
         gteps = nz / (spmm["ms"] / 1e3) / 1e9
+    # per-rank evidence for N > 1: devices, exchange init, halo size, exchange time
+    ranks = [rank_info]
+    exch = None
+    if world > 1:
+        ri = dict(rank_info, n_halo=info.n_halo,
+                  pack_ms_per_step=prof["pack"]["ms"] / a.steps)
+        ranks = [None] * world
+        dist.all_gather_object(ranks, ri)
+        exch = {"n_halo_max": max(r["n_halo"] for r in ranks),
+                "push_pull_ms_per_step_max": max(r["pack_ms_per_step"] for r in ranks),
+                "distinct_devices": len({r["uuid"] for r in ranks})}
     cpu = None
     if rank == 0 and world == 1 and not loop:   # the oracle baseline is timed at N=1 only
-        per, sample = oracle_sample_epoch_seconds(a.config, M, a.sample_frac or 0.1, 1, 1)
-        cpu = {"value": float(np.mean(per)), "unit": "s", "cores": cores(), "kind": "oracle",
-               "sample": sample}
+        per, sample, eff = oracle_sample_epoch_seconds(a.config, M, a.sample_frac or 0.1, 1, 1)
+        cpu = {"value": float(np.mean(per)), "unit": "s", "cores": eff,
+               "cores_available": cores(), "kind": "oracle", "sample": sample}
     if rank == 0:
         line = {
             "metric": METRIC, "value": step_s, "unit": "s", "n_gpus": world, "steps": a.steps,
@@ -439,6 +495,8 @@ def run_ours(a, rank, world, local):
                        "n_local": info.n_local, "n_halo": info.n_halo,
                        "nnz_local": info.nnz, "l2": "inputs larger than L2 (no flush needed)"},
             "roofline": roof,
+            "ranks": ranks,
+            "exchange": exch,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
@@ -462,20 +520,87 @@ def run_ours(a, rank, world, local):
         dist.destroy_process_group()
 
 
-def traffic_from_profiles(key):
-    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full
-    capture of the same workload (profiles/ncu_traffic.json), or None if not captured."""
-    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+NCU = "/usr/local/cuda/bin/ncu"
+
+
+def dram_probe(config, parts, rank, width, timeout=300):
+    """DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of ONE SpMM product of
+    width `width` on this build, this partition and this GPU: ncu profiles
+    tools/spmm_bench.py (a warm-up product, then the counted one; every column-slab launch
+    of the product summed).  Counters only -- no time from the profiled run is reported."""
+    if not os.path.exists(NCU):
+        return {"error": "ncu not found"}
+    with tempfile.TemporaryDirectory() as td:
+        log = os.path.join(td, "ncu.csv")
+        cmd = [NCU, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum",
+               "--kernel-name", "regex:k_spmm", "--print-units", "base", "--csv",
+               "--log-file", log, sys.executable, os.path.join(ROOT, "tools", "spmm_bench.py"),
+               "--config", config, "--parts", str(parts), "--rank", str(rank), "--widths",
+               str(width), "--iters", "1"]
+        try:
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout)
+        except Exception as ex:   # noqa: BLE001
+            return {"error": f"ncu run failed: {ex}"}
+        info = None
+        for ln in r.stdout.splitlines():
+            if ln.startswith("{"):
+                info = json.loads(ln)
+        if r.returncode != 0 or info is None or not os.path.exists(log):
+            return {"error": f"ncu rc={r.returncode}: {r.stderr[-300:]}"}
+        with open(log) as f:
+            lines = [ln for ln in f if ln.startswith('"')]
+        per, names = {}, {}
+        for row in csv.DictReader(lines):
+            try:
+                i = int(row["ID"])
+                per[i] = per.get(i, 0.0) + float(row["Metric Value"].replace(",", ""))
+                names[i] = row["Kernel Name"]
+            except (KeyError, ValueError):
+                continue
+        lpp = int(info["launches_per_product"])
+        ids = sorted(per)[-lpp:]
+        if len(ids) < lpp:
+            return {"error": f"ncu captured {len(per)} launches, expected >= {lpp}"}
+        return {"traffic": sum(per[i] for i in ids), "launches": lpp,
+                "kernels": sorted({names[i].split("(")[0] for i in ids}),
+                "alg_bytes": info["alg_bytes"], "how": "ncu --metrics dram__bytes_read.sum,"
+                "dram__bytes_write.sum on tools/spmm_bench.py (same build, same partition)"}
+
+
+def gather_roof(width):
+    """Best L2-resident (footprint <= 48 MB) random row-gather rate of the nearest measured
+    width from profiles/r2_gather_roof.jsonl (tools/gather_roof.cu on this pool's B200)."""
+    p = os.path.join(ROOT, "profiles", "r2_gather_roof.jsonl")
     try:
-        with open(p) as f:
-            return json.load(f).get(key)
+        rows = [json.loads(x) for x in open(p) if x.startswith("{")]
     except Exception:
         return None
+    rows = [r for r in rows if r.get("kind") == "gather" and r["footprint_mb"] <= 48]
+    if not rows:
+        return None
+    w = min({r["width"] for r in rows}, key=lambda x: abs(x - width))
+    return max((r for r in rows if r["width"] == w), key=lambda r: r["gbs"])
+
+
+def free_port():
+    s_ = socket.socket()
+    s_.bind(("127.0.0.1", 0))
+    port = s_.getsockname()[1]
+    s_.close()
+    return port
 
 
 def main():
     a = parse()
     rank, world, local = dist_env()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ and a.impl == "ours":
+        # one process per GPU: start the N ranks ourselves (same launch as the driver's)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={a.gpus}", "--master-addr", "127.0.0.1",
+               f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+        print(f"bench: --gpus {a.gpus} without WORLD_SIZE: launching {a.gpus} ranks: "
+              + " ".join(cmd[1:6]), file=sys.stderr, flush=True)
+        os.execv(sys.executable, cmd)
     if a.gpus != world and world > 1:
         print(f"warning: --gpus {a.gpus} but WORLD_SIZE {world}", file=sys.stderr)
     if a.impl == "reference":

@@ -323,6 +323,21 @@ digest_status digest_xent(const float* logits, int64_t n, int32_t C, int64_t ld,
  * comm == NULL or a 1-rank comm: only the scale is applied. */
 digest_status digest_grad_allreduce(digest_comm* comm, float* grads, int64_t count,
                                     float scale, void* stream);
+/* Fused weight-gradient + AGG on the peer transport (Alg. 1 line 13,
+ * P:233): digest_grad_slot returns the own window slot (count <= max_grad_count floats,
+ * device memory owned by the communicator) that the NEXT digest_grad_allreduce_ex call
+ * reduces; the caller makes it the G_W output of its digest_layer_bwd calls, so the
+ * split-K weight-gradient reduction writes the peer-visible slot directly (no publish
+ * copy).  digest_grad_allreduce_ex with DIGEST_AR_IN_SLOT then runs ONE kernel: signal
+ * this rank's slot ready to every peer, wait for theirs, grads <- scale * (slot_0 + ...
+ * + slot_{M-1}) in rank order (bit-identical to digest_grad_allreduce).  Without the
+ * flag it is digest_grad_allreduce.  Both: DIGEST_E_UNSUPPORTED unless `comm` is a
+ * connected peer communicator with more than one rank; DIGEST_E_SHAPE if count >
+ * max_grad_count. */
+enum { DIGEST_AR_IN_SLOT = 1u };
+digest_status digest_grad_slot(digest_comm* comm, float** slot_h);
+digest_status digest_grad_allreduce_ex(digest_comm* comm, float* grads, int64_t count,
+                                       float scale, uint32_t flags, void* stream);
 /* Loopback AGG for M partitions of one process: every buffer receives
  * scale * (bufs[0] + ... + bufs[n-1]) summed in index order. */
 digest_status digest_grad_allreduce_local(float* const* bufs_h, int32_t n, int64_t count,

@@ -85,6 +85,8 @@ _SIGS = {
     "digest_xent_workspace": ([_i64, _p], _i32),
     "digest_xent": ([_p, _i64, _i32, _i64, _p, _p, _f32, _p, _i64, _p, _p, _p], _i32),
     "digest_grad_allreduce": ([_p, _p, _i64, _f32, _p], _i32),
+    "digest_grad_allreduce_ex": ([_p, _p, _i64, _f32, _u32, _p], _i32),
+    "digest_grad_slot": ([_p, _p], _i32),
     "digest_grad_allreduce_local": ([_p, _i32, _i64, _f32, _p], _i32),
     "digest_sgd_step": ([_p, _p, _i64, _f32, _p], _i32),
     "digest_ps_mix": ([_p, _p, _i64, _f32, _p], _i32),
@@ -385,6 +387,21 @@ def digest_xent(logits, C_, labels, train_mask, w_loss, G_logits, loss_out, scra
 
 def digest_grad_allreduce(comm, grads, scale=1.0, stream=None):
     _check(lib.digest_grad_allreduce(comm, ptr(grads), grads.numel(), scale, stream_ptr(stream)))
+
+
+AR_IN_SLOT = 1
+
+
+def digest_grad_slot(comm) -> int:
+    """Device address of the own peer-window slot the next allreduce_ex reduces."""
+    p = C.c_void_p()
+    _check(lib.digest_grad_slot(comm, C.byref(p)))
+    return p.value
+
+
+def digest_grad_allreduce_ex(comm, grads, scale=1.0, flags=0, stream=None):
+    _check(lib.digest_grad_allreduce_ex(comm, ptr(grads), grads.numel(), scale, flags,
+                                        stream_ptr(stream)))
 
 
 def digest_grad_allreduce_local(bufs, scale=1.0, stream=None):

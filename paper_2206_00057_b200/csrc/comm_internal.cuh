@@ -56,8 +56,10 @@ struct FlagSet {             // *ptr[i] = value for i < n (fence.sys, st.release
 // One tiny launch: wait on `w`, then set `f` (either may be empty).
 digest_status flag_sync(const FlagWait& w, const FlagSet& f, cudaStream_t s);
 // AGG over the peer windows: g <- scale * sum_k g_k (rank order, bit-identical on all ranks).
-digest_status peer_allreduce(digest_comm* c, float* g, int64_t count, float scale, cudaStream_t s);
+digest_status peer_allreduce(digest_comm* c, float* g, int64_t count, float scale, cudaStream_t s,
+                             bool in_slot = false);
 void peer_comm_release(digest_comm* c);
+float* peer_next_slot(digest_comm* c);   // own slot of the next allreduce call
 }  // namespace dg
 
 // --- device helpers (included by the kernels that fuse their own wait/signal)

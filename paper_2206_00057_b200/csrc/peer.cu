@@ -38,9 +38,15 @@ struct SlotTable {
 
 // g[i] = scale * (slot_0[i] + slot_1[i] + ... + slot_{M-1}[i]), summed in rank order
 // exactly like the loopback k_sum_bufs (s = 0; s += b; s *= a).
+// `sig` (fused AGG, the slot was written by the weight-gradient kernels before this
+// launch in stream order): every block raises this rank's ready flag on every peer
+// (idempotent: same value) before waiting, so no block depends on another's schedule.
 __global__ void k_ar_reduce(float* __restrict__ g, int64_t n, SlotTable t, int nb, float a,
-                            dg::FlagWait w) {
-  if (threadIdx.x == 0) dg::wait_flags(w);
+                            dg::FlagWait w, dg::FlagSet sig) {
+  if (threadIdx.x == 0) {
+    if (sig.n) dg::set_flags(sig);
+    dg::wait_flags(w);
+  }
   __syncthreads();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -68,7 +74,7 @@ digest_status flag_sync(const FlagWait& w, const FlagSet& f, cudaStream_t s) {
 }
 
 digest_status peer_allreduce(digest_comm* c, float* g, int64_t count, float scale,
-                             cudaStream_t s) {
+                             cudaStream_t s, bool in_slot) {
   DG_ARG(c->connected, DIGEST_E_STATE, "peer communicator is not connected");
   DG_ARG(count <= c->max_grad, DIGEST_E_SHAPE,
          "allreduce of %lld floats exceeds the window's %lld", (long long)count,
@@ -81,8 +87,9 @@ digest_status peer_allreduce(digest_comm* c, float* g, int64_t count, float scal
   sig.n = M;
   sig.value = seq;
   for (int k = 0; k < M; ++k) sig.ptr[k] = win_i64(c->peer_win[k], kWinArReady) + c->rank;
-  DG_LAUNCH(DIGEST_PROF_OTHER, s, 8.0 * count, 0, k_ar_publish, blocks_for(count), 256, 0, g,
-            count, reinterpret_cast<float*>(c->win + slot_off), c->counters, sig);
+  if (!in_slot)
+    DG_LAUNCH(DIGEST_PROF_OTHER, s, 8.0 * count, 0, k_ar_publish, blocks_for(count), 256, 0, g,
+              count, reinterpret_cast<float*>(c->win + slot_off), c->counters, sig);
   FlagWait w{};
   w.n = M;
   w.value = seq;
@@ -92,13 +99,37 @@ digest_status peer_allreduce(digest_comm* c, float* g, int64_t count, float scal
     t.p[k] = reinterpret_cast<const float*>(c->peer_win[k] + slot_off);
   }
   DG_LAUNCH(DIGEST_PROF_OTHER, s, 4.0 * count * (M + 1), 0, k_ar_reduce, blocks_for(count), 256, 0,
-            g, count, t, M, scale, w);
+            g, count, t, M, scale, w, in_slot ? sig : FlagSet{});
   return DIGEST_OK;
+}
+
+// Own window slot of the NEXT allreduce call (parity of ar_seq + 1).
+float* peer_next_slot(digest_comm* c) {
+  const int par = (int)((c->ar_seq + 1) & 1);
+  return reinterpret_cast<float*>(c->win + kWinSlots +
+                                  sizeof(float) * (size_t)par * (size_t)c->max_grad);
 }
 
 }  // namespace dg
 
 extern "C" {
+
+digest_status digest_grad_slot(digest_comm* c, float** slot_h) {
+  DG_ARG(slot_h, DIGEST_E_INVALID, "NULL argument");
+  *slot_h = nullptr;
+  DG_ARG(dg::is_peer(c), DIGEST_E_UNSUPPORTED, "digest_grad_slot needs a multi-rank peer communicator");
+  DG_ARG(c->connected, DIGEST_E_STATE, "peer communicator is not connected");
+  *slot_h = dg::peer_next_slot(c);
+  return DIGEST_OK;
+}
+
+digest_status digest_grad_allreduce_ex(digest_comm* c, float* grads, int64_t count, float scale,
+                                       uint32_t flags, void* stream) {
+  if (!(flags & DIGEST_AR_IN_SLOT)) return digest_grad_allreduce(c, grads, count, scale, stream);
+  DG_ARG(grads && count >= 0, DIGEST_E_INVALID, "bad gradient buffer");
+  DG_ARG(dg::is_peer(c), DIGEST_E_UNSUPPORTED, "DIGEST_AR_IN_SLOT needs a multi-rank peer communicator");
+  return dg::peer_allreduce(c, grads, count, scale, dg::as_stream(stream), true);
+}
 
 digest_status digest_comm_init_peer(int32_t nranks, int32_t rank, int64_t max_grad_count,
                                     digest_comm** out_h) {

@@ -359,7 +359,10 @@ __global__ void __launch_bounds__(256, MB) k_spmm_rt(SpmmArgs a) {
 // chunk's (col, val) prefetched under the current gathers, and a warp-uniform exit from
 // the unrolled steps of a short chunk.  RAG: the slab is not a multiple of 4*LC floats
 // (the last float4 of a lane is predicated on the slab width).
-template <int LC, int VPL, int UNR, bool TWO, bool RAG, int MB>
+// XR (cross-row software pipelining): the next row's bounds load when a row starts and
+// its first (col, val) chunk loads under the current row's last gathers, so a row's
+// row_ptr -> col -> gather chain overlaps the previous row instead of following it.
+template <int LC, int VPL, int UNR, bool TWO, bool RAG, int MB, bool XR = false>
 __global__ void __launch_bounds__(256, MB) k_spmm_n(SpmmArgs a, const char* __restrict__ x0,
                                                     const char* __restrict__ x1m,
                                                     uint32_t split, uint32_t rb_half) {
@@ -372,17 +375,46 @@ __global__ void __launch_bounds__(256, MB) k_spmm_n(SpmmArgs a, const char* __re
   const int w4 = a.width >> 2;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  auto bounds = [&](int64_t r, int64_t& b, int64_t& e) {
+    b = e = 0;
+    if (r < a.n_rows) {
+      b = a.row_ptr[r];
+      e = a.in_len ? b + a.in_len[r] : a.row_ptr[r + 1];
+    }
+  };
+  int64_t beg, end;
+  int32_t c_nxt = 0;
+  float v_nxt = 0.f;
+  if (XR) {
+    bounds(warp, beg, end);
+    if (beg + lane < end) {
+      c_nxt = __ldg(a.col + beg + lane);
+      v_nxt = __ldg(a.val + beg + lane);
+    }
+  }
   for (int64_t row = warp; row < a.n_rows; row += nwarps) {
     float4 acc[VPL];
 #pragma unroll
     for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-    const int64_t beg = a.row_ptr[row];
-    const int64_t end = a.in_len ? beg + a.in_len[row] : a.row_ptr[row + 1];
-    int32_t c_nxt = 0;
-    float v_nxt = 0.f;
-    if (beg + lane < end) {
-      c_nxt = __ldg(a.col + beg + lane);
-      v_nxt = __ldg(a.val + beg + lane);
+    int64_t nbeg = 0, nend = 0;
+    if (XR) {
+      bounds(row + nwarps, nbeg, nend);
+      if (end <= beg) {   // empty row: its "last chunk" is the next row's first
+        c_nxt = 0;
+        v_nxt = 0.f;
+        if (nbeg + lane < nend) {
+          c_nxt = __ldg(a.col + nbeg + lane);
+          v_nxt = __ldg(a.val + nbeg + lane);
+        }
+      }
+    } else {
+      bounds(row, beg, end);
+      c_nxt = 0;
+      v_nxt = 0.f;
+      if (beg + lane < end) {
+        c_nxt = __ldg(a.col + beg + lane);
+        v_nxt = __ldg(a.val + beg + lane);
+      }
     }
     for (int64_t e0 = beg; e0 < end; e0 += 32) {
       const int32_t c = c_nxt;
@@ -390,9 +422,14 @@ __global__ void __launch_bounds__(256, MB) k_spmm_n(SpmmArgs a, const char* __re
       const int cnt = (int)min((int64_t)32, end - e0);
       c_nxt = 0;
       v_nxt = 0.f;
-      if (e0 + 32 + lane < end) {
-        c_nxt = __ldg(a.col + e0 + 32 + lane);
-        v_nxt = __ldg(a.val + e0 + 32 + lane);
+      if (e0 + 32 < end) {
+        if (e0 + 32 + lane < end) {
+          c_nxt = __ldg(a.col + e0 + 32 + lane);
+          v_nxt = __ldg(a.val + e0 + 32 + lane);
+        }
+      } else if (XR && nbeg + lane < nend) {   // last chunk: the next row's first
+        c_nxt = __ldg(a.col + nbeg + lane);
+        v_nxt = __ldg(a.val + nbeg + lane);
       }
 #pragma unroll
       for (int st = 0; st < STEPS; ++st) {
@@ -441,6 +478,10 @@ __global__ void __launch_bounds__(256, MB) k_spmm_n(SpmmArgs a, const char* __re
         acc[q].w += __shfl_down_sync(0xffffffffu, acc[q].w, off);
       }
     spmm_row_epilogue<LC, VPL>(a, row, lane, cl, g, w4, acc);
+    if (XR) {
+      beg = nbeg;
+      end = nend;
+    }
   }
 }
 
@@ -739,7 +780,7 @@ digest_status launch(const SpmmArgs& a, cudaStream_t s) {
 
 // Lean narrow-slab kernel launch (w4 = width/4 in 5..16).  Byte/flop accounting as in
 // launch(): the slab's share of the whole product's edge-gather bytes.
-template <int LC, int VPL, int UNR, bool RAG, int MB>
+template <int LC, int VPL, int UNR, bool RAG, int MB, bool XR = false>
 digest_status launch_n(const SpmmArgs& a, cudaStream_t s) {
   const double W = a.full_width > 0 ? a.full_width : a.width;
   const double frac = a.width / W;
@@ -751,14 +792,14 @@ digest_status launch_n(const SpmmArgs& a, cudaStream_t s) {
   const uint32_t rb_half = (uint32_t)(a.ld0 * 2);
   int64_t blocks = ceil_div(a.n_rows, 8);
   if (two) {
-    static const int64_t cap = resident_ctas(k_spmm_n<LC, VPL, UNR, true, RAG, MB>);
+    static const int64_t cap = resident_ctas(k_spmm_n<LC, VPL, UNR, true, RAG, MB, XR>);
     if (blocks > cap) blocks = cap;
-    DG_LAUNCH_TAG(DIGEST_PROF_SPMM, (int)W, s, bytes, flops, (k_spmm_n<LC, VPL, UNR, true, RAG, MB>),
+    DG_LAUNCH_TAG(DIGEST_PROF_SPMM, (int)W, s, bytes, flops, (k_spmm_n<LC, VPL, UNR, true, RAG, MB, XR>),
                   (unsigned)blocks, 256, 0, a, x0, x1m, (uint32_t)a.split, rb_half);
   } else {
-    static const int64_t cap = resident_ctas(k_spmm_n<LC, VPL, UNR, false, RAG, MB>);
+    static const int64_t cap = resident_ctas(k_spmm_n<LC, VPL, UNR, false, RAG, MB, XR>);
     if (blocks > cap) blocks = cap;
-    DG_LAUNCH_TAG(DIGEST_PROF_SPMM, (int)W, s, bytes, flops, (k_spmm_n<LC, VPL, UNR, false, RAG, MB>),
+    DG_LAUNCH_TAG(DIGEST_PROF_SPMM, (int)W, s, bytes, flops, (k_spmm_n<LC, VPL, UNR, false, RAG, MB, XR>),
                   (unsigned)blocks, 256, 0, a, x0, x1m, (uint32_t)INT32_MAX, rb_half);
   }
   return DIGEST_OK;
@@ -790,6 +831,10 @@ digest_status launch_narrow(const SpmmArgs& a, cudaStream_t s) {
   const int v = narrow_variant();
   if (w4 == 12) {
     switch (v) {
+      case 5: return launch_n<4, 3, 2, false, 4, true>(a, s);
+      case 6: return launch_n<4, 3, 1, false, 4, true>(a, s);
+      case 7: return launch_n<4, 3, 4, false, 3, true>(a, s);
+      case 8: return launch_n<4, 3, 4, false, 2, true>(a, s);
       case 2: return launch_n<4, 3, 4, false, 4>(a, s);
       case 3: return launch_n<4, 3, 2, false, 1>(a, s);
       case 4: return launch_n<4, 3, 1, false, 4>(a, s);
@@ -798,6 +843,10 @@ digest_status launch_narrow(const SpmmArgs& a, cudaStream_t s) {
   }
   if (w4 == 16) {
     switch (v) {
+      case 5: return launch_n<4, 4, 2, false, 4, true>(a, s);
+      case 6: return launch_n<8, 2, 4, false, 4, true>(a, s);
+      case 7: return launch_n<4, 4, 4, false, 2, true>(a, s);
+      case 8: return launch_n<8, 2, 4, false, 3, true>(a, s);
       case 2: return launch_n<4, 4, 4, false, 4>(a, s);
       case 3: return launch_n<8, 2, 4, false, 4>(a, s);
       case 4: return launch_n<4, 4, 1, false, 4>(a, s);

@@ -45,6 +45,8 @@ class TrainConfig:
     async_store: bool = False   # DIGEST-A on the peer transport: NOWAIT pushes, SNAPSHOT pulls
     store_bf16: bool = False    # bf16 stale store / transfers
     device_step: bool = False   # Adam step count on the device (CUDA-graph capturable epochs)
+    fused_agg: bool = True      # peer transport: weight gradients written straight into the
+                                # AGG window slot, one-kernel allreduce
 
     def __post_init__(self):
         hg = self.halo_grad
@@ -103,11 +105,17 @@ class DigestWorker:
         sizes = [dims[l] * dims[l + 1] for l in range(self.L)]
         self.W_flat = torch.empty(sum(sizes), dtype=torch.float32, device=dev)
         self.G_flat = torch.zeros_like(self.W_flat)
-        self.W, self.GW, off = [], [], 0
+        self.W, self.GW, self.gw_off, off = [], [], [], 0
         for l, s in enumerate(sizes):
             self.W.append(self.W_flat[off:off + s].view(dims[l], dims[l + 1]))
             self.GW.append(self.G_flat[off:off + s].view(dims[l], dims[l + 1]))
+            self.gw_off.append(off)
             off += s
+        # fused AGG (peer transport, M > 1): this epoch's G_W outputs live in the window slot
+        # (not in DIGEST-A, whose local step reads G_flat without an AGG)
+        self.fused_agg = bool(cfg.fused_agg and cfg.transport == "peer" and comm_grad is not None
+                              and part.num_parts > 1 and not cfg.async_store)
+        self._gw_out = None
         for w, src in zip(self.W, weights):
             w.copy_(torch.as_tensor(src, dtype=torch.float32))
         self.adam_m = self.adam_v = None
@@ -224,9 +232,10 @@ class DigestWorker:
         # G_in of layer l is produced already multiplied by 1[H^(l-1) > 0] (the 1-bit
         # mask of layer l-1), i.e. it is D^(l-1); layer l-1 then skips its own masking
         # pass (DIGEST_BWD_G_IS_D).
+        gw = self.GW[l - 1] if self._gw_out is None else self._gw_out[l - 1]
         D.digest_layer_bwd(self.part.handle, xl, xh, ldh, self.W[l - 1], dims[l - 1], dims[l],
                            act, self.layer_order(l), self.saved[l], None, self.G[l],
-                           self.GW[l - 1], self.G[l - 1] if l >= 2 else None, self.scratch,
+                           gw, self.G[l - 1] if l >= 2 else None, self.scratch,
                            stream, flags=(D.BWD_G_IS_D if l < self.L else 0) | hflags,
                            gin_mask=self.mask_bits[l - 1] if l >= 2 else None, G_halo=gh,
                            ld_gh=ldgh)
@@ -236,6 +245,9 @@ class DigestWorker:
         D.digest_return_halo_grad(self.store, l - 1, self.G[l - 1], self.H[l - 1], stream)
 
     def loss_and_backward(self, stream=None):
+        if self.fused_agg:   # G_W of every layer -> the slot the next AGG call reduces
+            slot = D.digest_grad_slot(self.comm_grad)
+            self._gw_out = [slot + 4 * o for o in self.gw_off]
         self.compute_loss(stream)
         for l in range(self.L, 0, -1):
             self.backward_layer(l, stream)
@@ -243,7 +255,11 @@ class DigestWorker:
                 self.return_halo_grad(l, stream)   # collective (NCCL) per level
 
     def allreduce(self, stream=None):
-        D.digest_grad_allreduce(self.comm_grad, self.G_flat, 1.0, stream)
+        if self._gw_out is not None:   # signal + rank-order sum, one kernel
+            D.digest_grad_allreduce_ex(self.comm_grad, self.G_flat, 1.0, D.AR_IN_SLOT, stream)
+            self._gw_out = None
+        else:
+            D.digest_grad_allreduce(self.comm_grad, self.G_flat, 1.0, stream)
 
     def update(self, stream=None):
         self.step_count += 1

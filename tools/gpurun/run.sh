@@ -21,14 +21,23 @@ for step in "$@"; do
     bench)  timeout 900 python bench.py > ${O}_bench.log 2>&1 ;;
     launches) timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none --csv \
               --log-file ${O}_launches.csv python bench.py --steps 2 --warmup 1 --no-e2e > ${O}_launches.log 2>&1 ;;
-    nsweep) for kv in "DIGEST_SPMM_N=0" "DIGEST_SPMM_N=1" "DIGEST_SPMM_N=2" "DIGEST_SPMM_N=3" "DIGEST_SPMM_N=4" \
-                      "DIGEST_SPMM_SMAX=64" "DIGEST_SPMM_SMAX=32" "DIGEST_SPMM_SMAX=48" "DIGEST_SPMM_SMAX=64 DIGEST_SPMM_N=3" ; do
-              echo "== $kv" >> ${O}_nsweep.log
-              env DIGEST_KNOBS=1 $kv timeout 300 python tools/spmm_bench.py --widths 256,100,48 --iters 5 >> ${O}_nsweep.log 2>&1
-              env DIGEST_KNOBS=1 $kv timeout 300 python tools/spmm_bench.py --parts 8 --widths 256,100,48 --iters 5 >> ${O}_nsweep.log 2>&1
+    nsweep) for kv in ${NSWEEP:-"DIGEST_SPMM_N=1" "DIGEST_SPMM_N=5" "DIGEST_SPMM_N=6" "DIGEST_SPMM_N=7" "DIGEST_SPMM_N=8"}; do
+              kvs=$(echo $kv | tr ',' ' ')
+              echo "== $kvs" >> ${O}_nsweep.log
+              env DIGEST_KNOBS=1 $kvs timeout 300 python tools/spmm_bench.py --widths ${NW:-256,100,48} --iters 5 >> ${O}_nsweep.log 2>&1
+              env DIGEST_KNOBS=1 $kvs timeout 300 python tools/spmm_bench.py --parts 8 --widths ${NW:-256,100,48} --iters 5 >> ${O}_nsweep.log 2>&1
             done ;;
     variants) timeout 1200 python -m pytest tests/test_gpu_spmm_variants.py -q -x -p no:cacheprovider > ${O}_variants.log 2>&1 ;;
     parity) timeout 1800 python -m pytest tests/test_gpu_parity.py -q -x -p no:cacheprovider > ${O}_parity.log 2>&1; echo "rc=$?" >> ${O}_parity.log ;;
+    oraclefull) timeout 1500 python tools/oracle_full_epoch.py --frac 1.0 > ${O}_oraclefull.log 2>&1
+                timeout 600 python tools/oracle_full_epoch.py --frac 0.1 >> ${O}_oraclefull.log 2>&1 ;;
+    ncun)   timeout 600 $NCU --set full --import-source on --clock-control none -k regex:k_spmm -s 1 -c 1 \
+              -o ${O}_ncu_w48 python tools/spmm_bench.py --widths 48 --iters 1 > ${O}_ncun.log 2>&1
+            env DIGEST_KNOBS=1 DIGEST_SPMM_SMAX=64 DIGEST_SPMM_N=3 timeout 600 $NCU --set full --import-source on \
+              --clock-control none -k regex:k_spmm -s 4 -c 1 -o ${O}_ncu_w256s64 \
+              python tools/spmm_bench.py --widths 256 --iters 1 >> ${O}_ncun.log 2>&1
+            env DIGEST_KNOBS=1 DIGEST_SPMM_N=0 timeout 600 $NCU --set full --import-source on --clock-control none \
+              -k regex:k_spmm -s 1 -c 1 -o ${O}_ncu_w48old python tools/spmm_bench.py --widths 48 --iters 1 >> ${O}_ncun.log 2>&1 ;;
     *)      echo "unknown step $step" >> ${O}_errors.log ;;
   esac
 done

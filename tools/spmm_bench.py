@@ -44,20 +44,26 @@ def main():
         xl = torch.rand(info.n_local, w, device="cuda")
         xh = torch.rand(max(info.n_halo, 1), w, device="cuda")
         y = torch.empty(max(rows, 1), w, device="cuda")
+        n0 = D.digest_launch_count()
         D.digest_propagate(p.handle, a.mode, xl, xh, w, w, y)
         torch.cuda.synchronize()
+        lpp = D.digest_launch_count() - n0
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
         e0.record()
-        for _ in range(a.iters):
+        for _ in range(max(a.iters, 0)):
             D.digest_propagate(p.handle, a.mode, xl, xh, w, w, y)
         e1.record()
         torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / a.iters
+        ms = e0.elapsed_time(e1) / max(a.iters, 1)
         alg = nnz * (8 + 4 * w) + rows * (4 * w + 8)
         print(json.dumps({"config": a.config, "parts": a.parts, "mode": a.mode, "width": w,
                           "ms": round(ms, 3), "gteps": round(nnz / ms / 1e6, 2),
                           "edge_gather_gbs": round(alg / ms / 1e6, 1),
-                          "slab": os.environ.get("DIGEST_SPMM_SLAB", "")}), flush=True)
+                          "launches_per_product": lpp, "nnz": nnz, "rows": rows,
+                          "src_rows": info.n_local + (info.n_halo if a.mode == 0 else 0),
+                          "alg_bytes": alg,
+                          "knobs": {k: v for k, v in os.environ.items()
+                                    if k.startswith("DIGEST_")}}), flush=True)
 
 
 if __name__ == "__main__":

@@ -40,7 +40,7 @@ class TrainConfig:
     #   '' / False / 'none'   halo inputs are constants (Eq. 6; default)
     #   'prev_epoch'          the paper's DIGEST backward: P_out^T D~^(t-1) W~^(t)T
     #   'same_epoch' / True   the exact variant: P_out^T D~^(t) W~^(t)T in the same iteration
-    halo_grad: object = 
+    halo_grad: object = ""
     transport: str = "nccl"     # multi-process exchange: 'nccl' or 'peer' (CUDA IPC windows)
     async_store: bool = False   # DIGEST-A on the peer transport: NOWAIT pushes, SNAPSHOT pulls
     store_bf16: bool = False    # bf16 stale store / transfers

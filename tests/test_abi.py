@@ -80,3 +80,21 @@ def test_peer_and_ps_argument_errors():
     assert L.digest_ps_upload_peer(None, None, 4, 0.5, None) == 3        # no connected window
     assert L.digest_delay(-1, None) == 1
     assert L.digest_store_create_ex(None, None, 0, None, 0, C.byref(out)) == 1
+
+
+def test_engine_imports_and_normalises_halo_grad():
+    """The host-side driver imports without a GPU; halo_grad accepts the documented forms."""
+    from paper_2206_00057_b200.engine import TrainConfig
+    mk = lambda hg: TrainConfig(dims=(4, 4), num_classes=2, halo_grad=hg).halo_grad
+    assert mk(True) == "same_epoch" and mk(False) == "" and mk("none") == ""
+    assert mk("prev_epoch") == "prev_epoch" and mk("same_epoch") == "same_epoch"
+    with pytest.raises(ValueError):
+        mk("later")
+
+
+def test_bench_module_imports():
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    m = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(m)
+    assert m.gather_roof(48)["gbs"] > 0 and callable(m.dram_probe)

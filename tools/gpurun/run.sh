@@ -31,13 +31,18 @@ for step in "$@"; do
     parity) timeout 1800 python -m pytest tests/test_gpu_parity.py -q -x -p no:cacheprovider > ${O}_parity.log 2>&1; echo "rc=$?" >> ${O}_parity.log ;;
     oraclefull) timeout 1500 python tools/oracle_full_epoch.py --frac 1.0 > ${O}_oraclefull.log 2>&1
                 timeout 600 python tools/oracle_full_epoch.py --frac 0.1 >> ${O}_oraclefull.log 2>&1 ;;
-    ncun)   timeout 600 $NCU --set full --import-source on --clock-control none -k regex:k_spmm -s 1 -c 1 \
-              -o ${O}_ncu_w48 python tools/spmm_bench.py --widths 48 --iters 1 > ${O}_ncun.log 2>&1
-            env DIGEST_KNOBS=1 DIGEST_SPMM_SMAX=64 DIGEST_SPMM_N=3 timeout 600 $NCU --set full --import-source on \
-              --clock-control none -k regex:k_spmm -s 4 -c 1 -o ${O}_ncu_w256s64 \
-              python tools/spmm_bench.py --widths 256 --iters 1 >> ${O}_ncun.log 2>&1
-            env DIGEST_KNOBS=1 DIGEST_SPMM_N=0 timeout 600 $NCU --set full --import-source on --clock-control none \
-              -k regex:k_spmm -s 1 -c 1 -o ${O}_ncu_w48old python tools/spmm_bench.py --widths 48 --iters 1 >> ${O}_ncun.log 2>&1 ;;
+    ncun)   for spec in "w48:48:1::" "w256s64:256:4:DIGEST_SPMM_SMAX=64:" "w48old:48:1:DIGEST_SPMM_N=0:" ${NCUN_EXTRA}; do
+              IFS=: read name wd skip kn _ <<< "$spec"
+              env DIGEST_KNOBS=1 $(echo $kn | tr ',' ' ') timeout 600 $NCU --set full --import-source on \
+                --clock-control none -k regex:k_spmm -s $skip -c 1 -o ${O}_ncu_$name \
+                python tools/spmm_bench.py --widths $wd --iters 1 >> ${O}_ncun.log 2>&1
+              $NCU -i ${O}_ncu_$name.ncu-rep --page raw --csv > ${O}_ncu_${name}_raw.csv 2>> ${O}_ncun.log
+              $NCU -i ${O}_ncu_$name.ncu-rep --page details --csv > ${O}_ncu_${name}_details.csv 2>> ${O}_ncun.log
+              $NCU -i ${O}_ncu_$name.ncu-rep --page source --csv > ${O}_ncu_${name}_source.csv 2>> ${O}_ncun.log
+              gzip -f ${O}_ncu_${name}_source.csv
+              rm -f ${O}_ncu_$name.ncu-rep
+            done ;;
+    full)   timeout 2400 python -m pytest tests/test_gpu_fullsize.py tests/test_gpu_halo_grad.py tests/test_gpu_async.py -q -x -s -p no:cacheprovider > ${O}_full.log 2>&1; echo "rc=$?" >> ${O}_full.log ;;
     *)      echo "unknown step $step" >> ${O}_errors.log ;;
   esac
 done

@@ -100,6 +100,7 @@ dg::SpmmArgs spmm_full(const digest_part* p, const float* X0, int64_t ld0, const
   a.ld0 = ld0;
   a.split = p->n_local;
   a.x0_rows = p->n_local;
+  a.csr_len = p->nnz;
   a.X1 = p->n_halo > 0 ? X1 : nullptr;   // no halo columns: a single-source product
   a.ld1 = ld1;
   a.Y = Y;
@@ -127,6 +128,7 @@ dg::SpmmArgs spmm_rh(const digest_part* p, const float* X, int64_t ld, float* Y,
   a.val = p->rh_val;
   a.n_rows = p->n_halo;
   a.nnz = p->rh_nnz;
+  a.csr_len = p->rh_nnz;
   a.X0 = X;
   a.ld0 = ld;
   a.split = INT64_MAX;

@@ -24,6 +24,9 @@ CASES += [(48, {"DIGEST_SPMM_PFH": "1", "DIGEST_SPMM_N": "0"}),
 # the lean narrow-slab kernel: every variant, ragged slabs, all three products
 CASES += [(w, {"DIGEST_SPMM_N": str(n)}) for w in (48, 64, 32) for n in (1, 2, 3, 4)]
 CASES += [(w, {"DIGEST_SPMM_N": "1", "MODE": m}) for w in (20, 36, 52, 48) for m in ("0", "1", "2")]
+# the CSR-tile-staged kernel (tiles whose range exceeds the staging capacity run direct)
+CASES += [(w, {"DIGEST_SPMM_N": str(n)}) for w in (48, 64) for n in (9, 10, 11, 12)]
+CASES += [(w, {"DIGEST_SPMM_N": "9", "MODE": m}) for w in (48, 64) for m in ("1", "2")]
 # column slabs of the lean kernel (balanced, <= SMAX floats)
 CASES += [(w, {"DIGEST_SPMM_SMAX": sm, "MODE": m}) for w, sm in ((100, "64"), (100, "48"),
                                                                   (256, "64"), (256, "32"),

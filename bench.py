@@ -415,6 +415,30 @@ def run_ours(a, rank, world, local):
         e2e = {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": 8, "input_pipeline": "double-buffered, copy stream"}
 
+    # ---- variant (same run, same workers): the exact layer-1 aggregation cache (SURVEY f3
+    # (i)).  Not the headline: it skips recomputing P_m X^(0) after the first epoch (valid
+    # only while the features are static; the paper recomputes layer 1 every epoch).
+    variants = {}
+    if (not a.cache_l1 and not a.graph and graph is None
+            and (cfg.dims[0] <= cfg.dims[1] or tc.order == D.ORDER_AGG_FIRST)):
+        for x in getattr(grp, "workers", [w]):
+            x.cfg.cache_l1, x._a1_ready = True, False
+        r += 1
+        grp.epoch(r)                       # aggregates A1 once
+        barrier()
+        v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        v0.record(stream)
+        for _ in range(a.steps):
+            r += 1
+            grp.epoch(r)
+        v1.record(stream)
+        barrier()
+        variants["cache_l1"] = {"ms_per_step": max_over_ranks(v0.elapsed_time(v1)) / a.steps,
+                                "note": "layer-1 aggregation A1 = P_m X^(0) computed once "
+                                        "(static features), exact"}
+        for x in getattr(grp, "workers", [w]):
+            x.cfg.cache_l1, x._a1_ready = False, False
+
     # ---- roofline of the dominant kernel: the SpMM product (all its column-slab launches)
     # of the width with the largest time.  HBM roof on the DRAM bytes ncu counts for one
     # such product of this build (dram_probe, run below after the timed regions), the
@@ -495,6 +519,7 @@ def run_ours(a, rank, world, local):
                        "n_local": info.n_local, "n_halo": info.n_halo,
                        "nnz_local": info.nnz, "l2": "inputs larger than L2 (no flush needed)"},
             "roofline": roof,
+            "variants": variants,
             "ranks": ranks,
             "exchange": exch,
             "cpu_baseline": cpu,

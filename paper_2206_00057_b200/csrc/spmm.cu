@@ -362,10 +362,15 @@ __global__ void __launch_bounds__(256, MB) k_spmm_rt(SpmmArgs a) {
 // XR (cross-row software pipelining): the next row's bounds load when a row starts and
 // its first (col, val) chunk loads under the current row's last gathers, so a row's
 // row_ptr -> col -> gather chain overlaps the previous row instead of following it.
-template <int LC, int VPL, int UNR, bool TWO, bool RAG, int MB, bool XR = false>
+// CH: the CSR streams (touched once) load with an L2 evict_first policy so they do not
+// displace the gathered source rows, which are reused by ~avg-degree rows.
+template <int LC, int VPL, int UNR, bool TWO, bool RAG, int MB, bool XR = false, bool CH = false>
 __global__ void __launch_bounds__(256, MB) k_spmm_n(SpmmArgs a, const char* __restrict__ x0,
                                                     const char* __restrict__ x1m,
                                                     uint32_t split, uint32_t rb_half) {
+  const uint64_t pol_s = CH ? policy_evict_first() : 0;
+  auto ldc = [&](const int32_t* p) { return CH ? ld_stream_i(p, pol_s) : __ldg(p); };
+  auto ldv = [&](const float* p) { return CH ? ld_stream_f(p, pol_s) : __ldg(p); };
   constexpr int EG = 32 / LC;
   constexpr int STEP = EG * UNR;
   constexpr int STEPS = (32 + STEP - 1) / STEP;
@@ -388,8 +393,8 @@ __global__ void __launch_bounds__(256, MB) k_spmm_n(SpmmArgs a, const char* __re
   if (XR) {
     bounds(warp, beg, end);
     if (beg + lane < end) {
-      c_nxt = __ldg(a.col + beg + lane);
-      v_nxt = __ldg(a.val + beg + lane);
+      c_nxt = ldc(a.col + beg + lane);
+      v_nxt = ldv(a.val + beg + lane);
     }
   }
   for (int64_t row = warp; row < a.n_rows; row += nwarps) {
@@ -403,8 +408,8 @@ __global__ void __launch_bounds__(256, MB) k_spmm_n(SpmmArgs a, const char* __re
         c_nxt = 0;
         v_nxt = 0.f;
         if (nbeg + lane < nend) {
-          c_nxt = __ldg(a.col + nbeg + lane);
-          v_nxt = __ldg(a.val + nbeg + lane);
+          c_nxt = ldc(a.col + nbeg + lane);
+          v_nxt = ldv(a.val + nbeg + lane);
         }
       }
     } else {
@@ -412,8 +417,8 @@ __global__ void __launch_bounds__(256, MB) k_spmm_n(SpmmArgs a, const char* __re
       c_nxt = 0;
       v_nxt = 0.f;
       if (beg + lane < end) {
-        c_nxt = __ldg(a.col + beg + lane);
-        v_nxt = __ldg(a.val + beg + lane);
+        c_nxt = ldc(a.col + beg + lane);
+        v_nxt = ldv(a.val + beg + lane);
       }
     }
     for (int64_t e0 = beg; e0 < end; e0 += 32) {
@@ -424,12 +429,12 @@ __global__ void __launch_bounds__(256, MB) k_spmm_n(SpmmArgs a, const char* __re
       v_nxt = 0.f;
       if (e0 + 32 < end) {
         if (e0 + 32 + lane < end) {
-          c_nxt = __ldg(a.col + e0 + 32 + lane);
-          v_nxt = __ldg(a.val + e0 + 32 + lane);
+          c_nxt = ldc(a.col + e0 + 32 + lane);
+          v_nxt = ldv(a.val + e0 + 32 + lane);
         }
       } else if (XR && nbeg + lane < nend) {   // last chunk: the next row's first
-        c_nxt = __ldg(a.col + nbeg + lane);
-        v_nxt = __ldg(a.val + nbeg + lane);
+        c_nxt = ldc(a.col + nbeg + lane);
+        v_nxt = ldv(a.val + nbeg + lane);
       }
 #pragma unroll
       for (int st = 0; st < STEPS; ++st) {
@@ -958,7 +963,7 @@ digest_status launch(const SpmmArgs& a, cudaStream_t s) {
 
 // Lean narrow-slab kernel launch (w4 = width/4 in 5..16).  Byte/flop accounting as in
 // launch(): the slab's share of the whole product's edge-gather bytes.
-template <int LC, int VPL, int UNR, bool RAG, int MB, bool XR = false>
+template <int LC, int VPL, int UNR, bool RAG, int MB, bool XR = false, bool CH = false>
 digest_status launch_n(const SpmmArgs& a, cudaStream_t s) {
   const double W = a.full_width > 0 ? a.full_width : a.width;
   const double frac = a.width / W;
@@ -970,14 +975,14 @@ digest_status launch_n(const SpmmArgs& a, cudaStream_t s) {
   const uint32_t rb_half = (uint32_t)(a.ld0 * 2);
   int64_t blocks = ceil_div(a.n_rows, 8);
   if (two) {
-    static const int64_t cap = resident_ctas(k_spmm_n<LC, VPL, UNR, true, RAG, MB, XR>);
+    static const int64_t cap = resident_ctas(k_spmm_n<LC, VPL, UNR, true, RAG, MB, XR, CH>);
     if (blocks > cap) blocks = cap;
-    DG_LAUNCH_TAG(DIGEST_PROF_SPMM, (int)W, s, bytes, flops, (k_spmm_n<LC, VPL, UNR, true, RAG, MB, XR>),
+    DG_LAUNCH_TAG(DIGEST_PROF_SPMM, (int)W, s, bytes, flops, (k_spmm_n<LC, VPL, UNR, true, RAG, MB, XR, CH>),
                   (unsigned)blocks, 256, 0, a, x0, x1m, (uint32_t)a.split, rb_half);
   } else {
-    static const int64_t cap = resident_ctas(k_spmm_n<LC, VPL, UNR, false, RAG, MB, XR>);
+    static const int64_t cap = resident_ctas(k_spmm_n<LC, VPL, UNR, false, RAG, MB, XR, CH>);
     if (blocks > cap) blocks = cap;
-    DG_LAUNCH_TAG(DIGEST_PROF_SPMM, (int)W, s, bytes, flops, (k_spmm_n<LC, VPL, UNR, false, RAG, MB, XR>),
+    DG_LAUNCH_TAG(DIGEST_PROF_SPMM, (int)W, s, bytes, flops, (k_spmm_n<LC, VPL, UNR, false, RAG, MB, XR, CH>),
                   (unsigned)blocks, 256, 0, a, x0, x1m, (uint32_t)INT32_MAX, rb_half);
   }
   return DIGEST_OK;
@@ -1018,16 +1023,6 @@ digest_status launch_t(const SpmmArgs& a, cudaStream_t s) {
   return DIGEST_OK;
 }
 
-// The lean kernel applies when the two sources share one row stride and every offset
-// fits 32 bits (source rows < 2^31, row bytes < 2^32).
-bool narrow_ok(const SpmmArgs& a) {
-  const int w4 = a.width / 4;
-  if (w4 < 5 || w4 > 16) return false;
-  const bool two = !(a.in_len != nullptr || a.X1 == nullptr || a.split >= INT32_MAX);
-  if (two && a.ld1 != a.ld0) return false;
-  return a.ld0 > 0 && a.ld0 * 2 < (int64_t)UINT32_MAX;
-}
-
 // DIGEST_SPMM_N (experiment switch): 0 = the round-1 kernels for narrow widths; 1..
 // variants of the lean kernel (default 1).
 int narrow_variant() {
@@ -1037,6 +1032,16 @@ int narrow_variant() {
     v = e ? atoi(e) : 1;
   }
   return v;
+}
+
+// The lean kernel applies when the two sources share one row stride and every offset
+// fits 32 bits (source rows < 2^31, row bytes < 2^32).
+bool narrow_ok(const SpmmArgs& a) {
+  const int w4 = a.width / 4;
+  if (w4 < 5 || w4 > (narrow_variant() >= 20 ? 32 : 16)) return false;
+  const bool two = !(a.in_len != nullptr || a.X1 == nullptr || a.split >= INT32_MAX);
+  if (two && a.ld1 != a.ld0) return false;
+  return a.ld0 > 0 && a.ld0 * 2 < (int64_t)UINT32_MAX;
 }
 
 digest_status launch_narrow(const SpmmArgs& a, cudaStream_t s) {
@@ -1049,6 +1054,7 @@ digest_status launch_narrow(const SpmmArgs& a, cudaStream_t s) {
       case 10: return launch_t<4, 3, 2, false, 64, 4096, 3>(a, s);
       case 11: return launch_t<4, 3, 4, false, 32, 3072, 3>(a, s);
       case 12: return launch_t<4, 3, 1, false, 32, 3072, 4>(a, s);
+      case 13: return launch_n<4, 3, 2, false, 4, false, true>(a, s);
       case 5: return launch_n<4, 3, 2, false, 4, true>(a, s);
       case 6: return launch_n<4, 3, 1, false, 4, true>(a, s);
       case 7: return launch_n<4, 3, 4, false, 3, true>(a, s);
@@ -1065,6 +1071,7 @@ digest_status launch_narrow(const SpmmArgs& a, cudaStream_t s) {
       case 10: return launch_t<8, 2, 4, false, 32, 3072, 4>(a, s);
       case 11: return launch_t<4, 4, 4, false, 32, 3072, 2>(a, s);
       case 12: return launch_t<8, 2, 2, false, 32, 3072, 4>(a, s);
+      case 13: return launch_n<4, 4, 2, false, 4, false, true>(a, s);
       case 5: return launch_n<4, 4, 2, false, 4, true>(a, s);
       case 6: return launch_n<8, 2, 4, false, 4, true>(a, s);
       case 7: return launch_n<4, 4, 4, false, 2, true>(a, s);
@@ -1078,6 +1085,14 @@ digest_status launch_narrow(const SpmmArgs& a, cudaStream_t s) {
   if (w4 == 8) {
     if (v == 3) return launch_n<8, 1, 4, false, 4>(a, s);
     return launch_n<4, 2, 2, false, 4>(a, s);
+  }
+  if (w4 > 16) {   // experiment (DIGEST_SPMM_N >= 20): w = 68..128 unslabbed
+    switch (v) {
+      case 21: return launch_n<8, 4, 2, true, 3>(a, s);
+      case 22: return launch_n<8, 4, 1, true, 4>(a, s);
+      case 23: return launch_n<4, 7, 1, true, 4>(a, s);
+      default: return launch_n<8, 4, 2, true, 2>(a, s);
+    }
   }
   if (w4 <= 7) return launch_n<4, 2, 2, true, 4>(a, s);
   if (w4 <= 11) return launch_n<4, 3, 2, true, 4>(a, s);

@@ -43,6 +43,8 @@ for step in "$@"; do
               rm -f ${O}_ncu_$name.ncu-rep
             done ;;
     full)   timeout 2400 python -m pytest tests/test_gpu_fullsize.py tests/test_gpu_halo_grad.py tests/test_gpu_async.py -q -x -s -p no:cacheprovider > ${O}_full.log 2>&1; echo "rc=$?" >> ${O}_full.log ;;
+    async_roof) nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -o tools/gather_async tools/gather_async.cu \
+              && timeout 900 tools/gather_async > ${O}_async_roof.jsonl 2> ${O}_async_roof.err ;;
     *)      echo "unknown step $step" >> ${O}_errors.log ;;
   esac
 done

@@ -91,6 +91,15 @@ digest_status digest_comm_destroy(digest_comm* comm);
  * consumers spin on them inside their kernels (a wait longer than 30 s traps the
  * kernel: a CUDA error instead of a hang).  Every rank must issue the same sequence
  * of collective calls (push/pull/return per level, allreduce). */
+/* The boundary exchange primitive of the NCCL transport (push; halo-gradient
+ * return): grouped ncclSend/ncclRecv, send_h[k] (count_s_h[k] floats, device) to rank
+ * k and recv_h[k] (count_r_h[k] floats, device) from rank k, for every k with a
+ * non-zero count -- the own rank included (a self transfer), so a 1-rank communicator
+ * runs the same NCCL calls as a multi-rank one.  Host arrays have nranks entries.
+ * DIGEST_E_INVALID for a peer-memory communicator; DIGEST_E_NCCL on NCCL errors. */
+digest_status digest_comm_alltoallv(digest_comm* comm, const float* const* send_h,
+                                    const int64_t* count_s_h, float* const* recv_h,
+                                    const int64_t* count_r_h, void* stream);
 #define DIGEST_IPC_HANDLE_BYTES 64
 digest_status digest_comm_init_peer(int32_t nranks, int32_t rank, int64_t max_grad_count,
                                     digest_comm** out_h);
@@ -320,7 +329,8 @@ digest_status digest_xent(const float* logits, int64_t n, int32_t C, int64_t ld,
  * peer communicator: publish into the own window, then every rank sums all ranks'
  * slots in rank order with the scale fused -- bit-identical to
  * digest_grad_allreduce_local on the same buffers; count <= max_grad_count).
- * comm == NULL or a 1-rank comm: only the scale is applied. */
+ * comm == NULL or a 1-rank peer comm: only the scale is applied (a 1-rank NCCL comm
+ * still runs ncclAllReduce, a copy, so that path is exercised on one GPU). */
 digest_status digest_grad_allreduce(digest_comm* comm, float* grads, int64_t count,
                                     float scale, void* stream);
 /* Fused weight-gradient + AGG on the peer transport (Alg. 1 line 13,

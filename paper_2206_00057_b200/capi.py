@@ -87,6 +87,7 @@ _SIGS = {
     "digest_grad_allreduce": ([_p, _p, _i64, _f32, _p], _i32),
     "digest_grad_allreduce_ex": ([_p, _p, _i64, _f32, _u32, _p], _i32),
     "digest_grad_slot": ([_p, _p], _i32),
+    "digest_comm_alltoallv": ([_p, _p, _p, _p, _p, _p], _i32),
     "digest_grad_allreduce_local": ([_p, _i32, _i64, _f32, _p], _i32),
     "digest_sgd_step": ([_p, _p, _i64, _f32, _p], _i32),
     "digest_ps_mix": ([_p, _p, _i64, _f32, _p], _i32),
@@ -390,6 +391,16 @@ def digest_grad_allreduce(comm, grads, scale=1.0, stream=None):
 
 
 AR_IN_SLOT = 1
+
+
+def digest_comm_alltoallv(comm, sends, recvs, stream=None):
+    """sends / recvs: per-rank float tensors (or None); counts are their numel()."""
+    n = len(sends)
+    sp = (C.c_void_p * n)(*[ptr(t) for t in sends])
+    rp = (C.c_void_p * n)(*[ptr(t) for t in recvs])
+    cs = (C.c_int64 * n)(*[0 if t is None else t.numel() for t in sends])
+    cr = (C.c_int64 * n)(*[0 if t is None else t.numel() for t in recvs])
+    _check(lib.digest_comm_alltoallv(comm, sp, cs, rp, cr, stream_ptr(stream)))
 
 
 def digest_grad_slot(comm) -> int:

@@ -26,8 +26,7 @@ digest_status comm_alltoallv(digest_comm* c, const float* const* send, const int
                              float* const* recv, const int64_t* count_r, cudaStream_t s,
                              ncclDataType_t dt) {
   DG_NCCL(ncclGroupStart());
-  for (int k = 0; k < c->nranks; ++k) {
-    if (k == c->rank) continue;
+  for (int k = 0; k < c->nranks; ++k) {   // own rank included: a self transfer if counted
     if (count_s[k] > 0) {
       ncclResult_t r = ncclSend(send[k], (size_t)count_s[k], dt, k, c->comm, s);
       if (r != ncclSuccess) {
@@ -77,6 +76,19 @@ digest_status digest_comm_init(const uint8_t id_h[128], int32_t nranks, int32_t 
   }
   *out_h = c;
   return DIGEST_OK;
+}
+
+digest_status digest_comm_alltoallv(digest_comm* c, const float* const* send_h,
+                                    const int64_t* count_s_h, float* const* recv_h,
+                                    const int64_t* count_r_h, void* stream) {
+  DG_ARG(c && send_h && count_s_h && recv_h && count_r_h, DIGEST_E_INVALID, "NULL argument");
+  DG_ARG(c->kind == 0, DIGEST_E_INVALID, "not an NCCL communicator");
+  for (int k = 0; k < c->nranks; ++k) {
+    DG_ARG(count_s_h[k] >= 0 && count_r_h[k] >= 0, DIGEST_E_INVALID, "negative count");
+    DG_ARG(!count_s_h[k] || send_h[k], DIGEST_E_INVALID, "NULL send buffer %d", k);
+    DG_ARG(!count_r_h[k] || recv_h[k], DIGEST_E_INVALID, "NULL recv buffer %d", k);
+  }
+  return dg::comm_alltoallv(c, send_h, count_s_h, recv_h, count_r_h, dg::as_stream(stream));
 }
 
 digest_status digest_comm_destroy(digest_comm* c) {

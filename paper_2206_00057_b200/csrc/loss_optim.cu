@@ -233,7 +233,7 @@ digest_status digest_grad_allreduce(digest_comm* comm, float* grads, int64_t cou
   DG_ARG(grads && count >= 0, DIGEST_E_INVALID, "bad gradient buffer");
   cudaStream_t s = dg::as_stream(stream);
   if (dg::is_peer(comm)) return dg::peer_allreduce(comm, grads, count, scale, s);  // scale fused
-  if (comm && comm->nranks > 1) DG_TRY(dg::comm_allreduce_sum(comm, grads, count, s));
+  if (comm && comm->kind == 0) DG_TRY(dg::comm_allreduce_sum(comm, grads, count, s));
   if (scale != 1.0f && count > 0)
     DG_LAUNCH(DIGEST_PROF_OTHER, s, 8.0 * count, 0, k_scale, elt_blocks(count), 256, 0, grads,
               count, scale);

@@ -490,184 +490,6 @@ __global__ void __launch_bounds__(256, MB) k_spmm_n(SpmmArgs a, const char* __re
   }
 }
 
-// ---------------------------------------------------------------------------------------
-// CSR-tile-staged narrow kernel (k_spmm_t).  The row_ptr -> (col, val) -> gather chain
-// of every row is cut: a persistent CTA walks tiles of TR consecutive rows (tile t =
-// blockIdx.x + k*gridDim.x, so the rows in flight chip-wide stay one narrow window) and
-// stages the NEXT tile's (col, val) range into shared memory with cp.async while its
-// warps gather for the current one; the tile after that has its row_ptr already in
-// registers.  Warps grab the tile's rows dynamically (shared counter: balanced to one
-// row) and read each edge's (col, val) from shared memory (broadcast LDS), so the only
-// global latency on a row's critical path is its gathers.  Lane layout and epilogue as
-// k_spmm_n.  A tile whose range exceeds CAP entries (hub rows) is processed from global
-// memory by the same warps (no staging).
-__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(tc::smem_u32(dst)),
-               "l"(src), "r"(src_bytes)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
-
-template <int TR, int CAP>
-struct TileSmem {
-  int32_t col[2][CAP + 8];   // 4 of alignment slack + 4 of chunk rounding
-  float val[2][CAP + 8];
-  int64_t rp[2][TR + 1];   // row_ptr of the tile's rows (global offsets)
-  int32_t ln[2][TR];       // in_len (P_in products) or row lengths
-  int64_t base[2];         // global offset of col[b][0] (range start aligned down to 4)
-  int32_t staged[2];       // 1: range fits CAP and was staged
-  int32_t next[2];         // dynamic row counter
-};
-
-template <int LC, int VPL, int UNR, bool TWO, bool RAG, int TR, int CAP, int MB>
-__global__ void __launch_bounds__(256, MB) k_spmm_t(SpmmArgs a, const char* __restrict__ x0,
-                                                    const char* __restrict__ x1m,
-                                                    uint32_t split, uint32_t rb_half,
-                                                    int64_t csr_len) {
-  constexpr int EG = 32 / LC;
-  constexpr int STEP = EG * UNR;
-  extern __shared__ __align__(16) uint8_t smem_t[];
-  TileSmem<TR, CAP>& S = *reinterpret_cast<TileSmem<TR, CAP>*>(smem_t);
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int cl = lane % LC, g = lane / LC;
-  const int w4 = a.width >> 2;
-  const int64_t ntiles = (a.n_rows + TR - 1) / TR;
-
-  // row_ptr (+ in_len) of a tile into registers of threads 0..TR
-  auto load_rp = [&](int64_t t, int64_t& rpv, int32_t& lnv) {
-    rpv = 0;
-    lnv = 0;
-    if (t < ntiles && tid <= TR) {
-      const int64_t r = t * TR + tid;
-      const int64_t rr = r < a.n_rows ? r : a.n_rows;
-      rpv = a.row_ptr[rr];
-      if (tid < TR && r < a.n_rows)
-        lnv = a.in_len ? a.in_len[r] : (int32_t)(a.row_ptr[r + 1] - rpv);
-    }
-  };
-  // rp/ln registers of tile t -> shared buffer b, then (after a barrier) stage its range
-  auto publish = [&](int b, int64_t rpv, int32_t lnv) {
-    if (tid <= TR) S.rp[b][tid] = rpv;
-    if (tid < TR) S.ln[b][tid] = lnv;
-    if (tid == 0) S.next[b] = 0;
-  };
-  auto stage = [&](int64_t t, int b) {
-    if (t >= ntiles) return;
-    const int nr = (int)min((int64_t)TR, a.n_rows - t * TR);
-    const int64_t beg = S.rp[b][0] & ~(int64_t)3;
-    const int64_t end = S.rp[b][nr];
-    const bool fits = end - beg <= CAP;
-    if (tid == 0) {
-      S.base[b] = beg;
-      S.staged[b] = fits;
-    }
-    if (!fits) return;
-    const int nchunk = (int)((end - beg + 3) >> 2);   // 16-byte chunks per array
-    for (int i = tid; i < 2 * nchunk; i += blockDim.x) {
-      const int k = i < nchunk ? i : i - nchunk;
-      const int64_t e = beg + 4 * (int64_t)k;
-      const int64_t left = csr_len - e;
-      const int bytes = left >= 4 ? 16 : (left > 0 ? (int)left * 4 : 0);
-      if (i < nchunk)
-        cp_async16(&S.col[b][4 * k], bytes ? (const void*)(a.col + e) : (const void*)a.col, bytes);
-      else
-        cp_async16(&S.val[b][4 * k], bytes ? (const void*)(a.val + e) : (const void*)a.val, bytes);
-    }
-  };
-
-  // one row: edges [lb, lb + len) of the staged arrays (cs, vs) or of global memory
-  auto do_row = [&](int64_t row, const int32_t* cs, const float* vs, int64_t lb, int len) {
-    float4 acc[VPL];
-#pragma unroll
-    for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int e0 = 0; e0 < len; e0 += STEP) {
-      float4 t[UNR][VPL];
-      float x[UNR];
-      const float4* p[UNR];
-      const bool full = e0 + STEP <= len;   // warp-uniform
-#pragma unroll
-      for (int u = 0; u < UNR; ++u) {
-        const int j = e0 + u * EG + g;
-        uint32_t cr = 0u;   // past the row: source row 0 (valid), weight 0
-        x[u] = 0.f;
-        if (full || j < len) {
-          cr = (uint32_t)cs[lb + j];
-          x[u] = vs[lb + j];
-        }
-        const char* bs = x0;
-        if (TWO) bs = (cr & 0x7fffffffu) >= split ? x1m : x0;
-        p[u] = reinterpret_cast<const float4*>(bs + (uint64_t)(cr << 1) * rb_half);
-      }
-#pragma unroll
-      for (int u = 0; u < UNR; ++u)
-#pragma unroll
-        for (int q = 0; q < VPL; ++q) {
-          const int idx = cl + q * LC;
-          t[u][q] = __ldg(p[u] + (RAG && q == VPL - 1 ? min(idx, w4 - 1) : idx));
-        }
-#pragma unroll
-      for (int u = 0; u < UNR; ++u)
-#pragma unroll
-        for (int q = 0; q < VPL; ++q) {
-          acc[q].x = fmaf(x[u], t[u][q].x, acc[q].x);
-          acc[q].y = fmaf(x[u], t[u][q].y, acc[q].y);
-          acc[q].z = fmaf(x[u], t[u][q].z, acc[q].z);
-          acc[q].w = fmaf(x[u], t[u][q].w, acc[q].w);
-        }
-    }
-#pragma unroll
-    for (int off = LC; off < 32; off <<= 1)
-#pragma unroll
-      for (int q = 0; q < VPL; ++q) {
-        acc[q].x += __shfl_down_sync(0xffffffffu, acc[q].x, off);
-        acc[q].y += __shfl_down_sync(0xffffffffu, acc[q].y, off);
-        acc[q].z += __shfl_down_sync(0xffffffffu, acc[q].z, off);
-        acc[q].w += __shfl_down_sync(0xffffffffu, acc[q].w, off);
-      }
-    spmm_row_epilogue<LC, VPL>(a, row, lane, cl, g, w4, acc);
-  };
-
-  int64_t t = blockIdx.x;
-  int b = 0;
-  int64_t rpv;
-  int32_t lnv;
-  load_rp(t, rpv, lnv);                       // tile t -> registers -> buffer 0, staged
-  publish(0, rpv, lnv);
-  __syncthreads();
-  stage(t, 0);
-  cp_async_commit();
-  load_rp(t + gridDim.x, rpv, lnv);           // registers hold the next tile's row_ptr
-  for (; t < ntiles; t += gridDim.x, b ^= 1) {
-    const int64_t tn = t + gridDim.x;
-    __syncthreads();                          // every warp is done with buffer b^1
-    publish(b ^ 1, rpv, lnv);
-    load_rp(tn + gridDim.x, rpv, lnv);        // two tiles ahead, consumed next iteration
-    __syncthreads();
-    stage(tn, b ^ 1);
-    cp_async_commit();
-    cp_async_wait1();                         // this thread's copies of tile t have landed
-    __syncthreads();                          // ... and every thread's
-    const int nr = (int)min((int64_t)TR, a.n_rows - t * TR);
-    const bool staged = S.staged[b];
-    const int64_t base = S.base[b];
-    for (;;) {
-      int r = 0;
-      if (lane == 0) r = atomicAdd(&S.next[b], 1);
-      r = __shfl_sync(0xffffffffu, r, 0);
-      if (r >= nr) break;
-      const int64_t row = t * TR + r;
-      const int64_t beg = S.rp[b][r];
-      const int len = S.ln[b][r];
-      if (staged)
-        do_row(row, S.col[b], S.val[b], beg - base, len);
-      else
-        do_row(row, a.col, a.val, beg, len);
-    }
-  }
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-}
-
 // Single-source product through TMA row gathers (tile::gather4), experimental
 // (DIGEST_SPMM_TMA=1; measured 1.45-1.6x SLOWER than the load-based kernels at w=48/100,
 // products M=1 and 8 parts -- profiles/r1_spmm_variant_sweep.log -- so it is off).  Warp per row as above, but the 32 gathered rows of a (col, val)
@@ -988,43 +810,9 @@ digest_status launch_n(const SpmmArgs& a, cudaStream_t s) {
   return DIGEST_OK;
 }
 
-// CSR-tile-staged kernel launch (k_spmm_t); same accounting as launch_n.
-template <int LC, int VPL, int UNR, bool RAG, int TR, int CAP, int MB>
-digest_status launch_t(const SpmmArgs& a, cudaStream_t s) {
-  const double W = a.full_width > 0 ? a.full_width : a.width;
-  const double frac = a.width / W;
-  const double bytes = frac * ((double)a.nnz * (8.0 + 4.0 * W) + (double)a.n_rows * (4.0 * W + 8.0));
-  const double flops = 2.0 * (double)a.nnz * a.width;
-  const bool two = !(a.in_len != nullptr || a.X1 == nullptr || a.split >= INT32_MAX);
-  const char* x0 = reinterpret_cast<const char*>(a.X0);
-  const char* x1m = two ? reinterpret_cast<const char*>(a.X1) - a.split * a.ld1 * 4 : x0;
-  const uint32_t rb_half = (uint32_t)(a.ld0 * 2);
-  const int smem = (int)sizeof(TileSmem<TR, CAP>);
-  const int64_t ntiles = ceil_div(a.n_rows, TR);
-#define DG_LAUNCH_T(TWO_)                                                                        \
-  do {                                                                                           \
-    auto kern = k_spmm_t<LC, VPL, UNR, TWO_, RAG, TR, CAP, MB>;                                  \
-    static int64_t cap = 0;                                                                      \
-    if (cap == 0) {                                                                              \
-      DG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));    \
-      int per_sm = 0;                                                                            \
-      DG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));          \
-      cap = (int64_t)(per_sm < 1 ? 1 : per_sm) * num_sms();                                      \
-    }                                                                                            \
-    const int64_t blocks = ntiles < cap ? ntiles : cap;                                          \
-    DG_LAUNCH_TAG(DIGEST_PROF_SPMM, (int)W, s, bytes, flops, kern, (unsigned)blocks, 256, smem, a, \
-                  x0, x1m, (uint32_t)(two ? a.split : INT32_MAX), rb_half, a.csr_len);           \
-  } while (0)
-  if (two)
-    DG_LAUNCH_T(true);
-  else
-    DG_LAUNCH_T(false);
-#undef DG_LAUNCH_T
-  return DIGEST_OK;
-}
-
-// DIGEST_SPMM_N (experiment switch): 0 = the round-1 kernels for narrow widths; 1..
-// variants of the lean kernel (default 1).
+// DIGEST_SPMM_N (experiment switch): 0 = the round-1 kernels for narrow widths;
+// 1 = default lean kernel; 2 = cross-row pipelined, 32 gathers per group step (fewer
+// warps); 3 = default without the CSR evict_first policy (profiles/r2_spmm_sweep.md).
 int narrow_variant() {
   static int v = -2;
   if (v == -2) {
@@ -1038,7 +826,7 @@ int narrow_variant() {
 // fits 32 bits (source rows < 2^31, row bytes < 2^32).
 bool narrow_ok(const SpmmArgs& a) {
   const int w4 = a.width / 4;
-  if (w4 < 5 || w4 > (narrow_variant() >= 20 ? 32 : 16)) return false;
+  if (w4 < 5 || w4 > 32) return false;
   const bool two = !(a.in_len != nullptr || a.X1 == nullptr || a.split >= INT32_MAX);
   if (two && a.ld1 != a.ld0) return false;
   return a.ld0 > 0 && a.ld0 * 2 < (int64_t)UINT32_MAX;
@@ -1046,57 +834,27 @@ bool narrow_ok(const SpmmArgs& a) {
 
 digest_status launch_narrow(const SpmmArgs& a, cudaStream_t s) {
   const int w4 = a.width / 4;
-  int v = narrow_variant();
-  if (v >= 9 && a.csr_len <= 0) v = 1;   // the CSR-tile kernel needs the array length
+  const int v = narrow_variant();
+  // measured, products-shaped partitions (profiles/r2_spmm_sweep.md): w=48 M=1 3.86 ->
+  // 2.97 ms, M=8 0.52 -> 0.46 ms; w=100 7.23 -> 6.38 ms
   if (w4 == 12) {
-    switch (v) {
-      case 9: return launch_t<4, 3, 2, false, 32, 3072, 4>(a, s);
-      case 10: return launch_t<4, 3, 2, false, 64, 4096, 3>(a, s);
-      case 11: return launch_t<4, 3, 4, false, 32, 3072, 3>(a, s);
-      case 12: return launch_t<4, 3, 1, false, 32, 3072, 4>(a, s);
-      case 13: return launch_n<4, 3, 2, false, 4, false, true>(a, s);
-      case 5: return launch_n<4, 3, 2, false, 4, true>(a, s);
-      case 6: return launch_n<4, 3, 1, false, 4, true>(a, s);
-      case 7: return launch_n<4, 3, 4, false, 3, true>(a, s);
-      case 8: return launch_n<4, 3, 4, false, 2, true>(a, s);
-      case 2: return launch_n<4, 3, 4, false, 4>(a, s);
-      case 3: return launch_n<4, 3, 2, false, 1>(a, s);
-      case 4: return launch_n<4, 3, 1, false, 4>(a, s);
-      default: return launch_n<4, 3, 2, false, 4>(a, s);
-    }
+    if (v == 2) return launch_n<4, 3, 4, false, 3, true, true>(a, s);
+    if (v == 3) return launch_n<4, 3, 2, false, 4>(a, s);
+    return launch_n<4, 3, 2, false, 4, false, true>(a, s);
   }
   if (w4 == 16) {
-    switch (v) {
-      case 9: return launch_t<4, 4, 2, false, 32, 3072, 4>(a, s);
-      case 10: return launch_t<8, 2, 4, false, 32, 3072, 4>(a, s);
-      case 11: return launch_t<4, 4, 4, false, 32, 3072, 2>(a, s);
-      case 12: return launch_t<8, 2, 2, false, 32, 3072, 4>(a, s);
-      case 13: return launch_n<4, 4, 2, false, 4, false, true>(a, s);
-      case 5: return launch_n<4, 4, 2, false, 4, true>(a, s);
-      case 6: return launch_n<8, 2, 4, false, 4, true>(a, s);
-      case 7: return launch_n<4, 4, 4, false, 2, true>(a, s);
-      case 8: return launch_n<8, 2, 4, false, 3, true>(a, s);
-      case 2: return launch_n<4, 4, 4, false, 4>(a, s);
-      case 3: return launch_n<8, 2, 4, false, 4>(a, s);
-      case 4: return launch_n<4, 4, 1, false, 4>(a, s);
-      default: return launch_n<4, 4, 2, false, 4>(a, s);
-    }
+    if (v == 2) return launch_n<8, 2, 4, false, 3, true, true>(a, s);
+    if (v == 3) return launch_n<4, 4, 2, false, 4>(a, s);
+    return launch_n<4, 4, 2, false, 4, false, true>(a, s);
   }
-  if (w4 == 8) {
-    if (v == 3) return launch_n<8, 1, 4, false, 4>(a, s);
-    return launch_n<4, 2, 2, false, 4>(a, s);
-  }
-  if (w4 > 16) {   // experiment (DIGEST_SPMM_N >= 20): w = 68..128 unslabbed
-    switch (v) {
-      case 21: return launch_n<8, 4, 2, true, 3>(a, s);
-      case 22: return launch_n<8, 4, 1, true, 4>(a, s);
-      case 23: return launch_n<4, 7, 1, true, 4>(a, s);
-      default: return launch_n<8, 4, 2, true, 2>(a, s);
-    }
-  }
-  if (w4 <= 7) return launch_n<4, 2, 2, true, 4>(a, s);
-  if (w4 <= 11) return launch_n<4, 3, 2, true, 4>(a, s);
-  return launch_n<4, 4, 2, true, 4>(a, s);
+  if (w4 == 8) return launch_n<4, 2, 2, false, 4, false, true>(a, s);
+  if (w4 <= 7) return launch_n<4, 2, 2, true, 4, false, true>(a, s);
+  if (w4 <= 11) return launch_n<4, 3, 2, true, 4, false, true>(a, s);
+  if (w4 <= 15) return launch_n<4, 4, 2, true, 4, false, true>(a, s);
+  // w = 68..128 (products d0 = 100: 25 float4 on 8 lanes x 4, ragged)
+  if (v == 2) return launch_n<8, 4, 2, true, 3, true, true>(a, s);
+  if (v == 3) return launch_n<8, 4, 2, true, 3>(a, s);
+  return launch_n<8, 4, 2, true, 3, false, true>(a, s);
 }
 
 }  // namespace

@@ -21,16 +21,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CASES = [(48, {"DIGEST_SPMM_V12": str(v), "DIGEST_SPMM_N": "0"}) for v in range(8)]
 CASES += [(48, {"DIGEST_SPMM_PFH": "1", "DIGEST_SPMM_N": "0"}),
           (48, {"DIGEST_SPMM_GRID": "1", "DIGEST_SPMM_N": "0"})]
-# the lean narrow-slab kernel: every variant, ragged slabs, all three products
-CASES += [(w, {"DIGEST_SPMM_N": str(n)}) for w in (48, 64, 32) for n in (1, 2, 3, 4)]
-CASES += [(w, {"DIGEST_SPMM_N": "1", "MODE": m}) for w in (20, 36, 52, 48) for m in ("0", "1", "2")]
-# the CSR-tile-staged kernel (tiles whose range exceeds the staging capacity run direct)
-CASES += [(w, {"DIGEST_SPMM_N": str(n)}) for w in (48, 64) for n in (9, 10, 11, 12)]
-CASES += [(w, {"DIGEST_SPMM_N": "9", "MODE": m}) for w in (48, 64) for m in ("1", "2")]
-# lean kernel with L2 evict_first CSR loads; unslabbed w = 68..128 experiments
-CASES += [(w, {"DIGEST_SPMM_N": "13"}) for w in (48, 64)]
-CASES += [(w, {"DIGEST_SPMM_N": str(n), "MODE": m}) for w in (100, 128) for n in (20, 21, 22, 23)
-          for m in ("0",)] + [(100, {"DIGEST_SPMM_N": "20", "MODE": m}) for m in ("1", "2")]
+# the lean narrow kernel: every variant, ragged widths, all three products
+CASES += [(w, {"DIGEST_SPMM_N": str(n)}) for w in (48, 64, 100, 128) for n in (1, 2, 3)]
+CASES += [(w, {"DIGEST_SPMM_N": "1", "MODE": m}) for w in (20, 32, 36, 52, 48, 100)
+          for m in ("0", "1", "2")]
 # column slabs of the lean kernel (balanced, <= SMAX floats)
 CASES += [(w, {"DIGEST_SPMM_SMAX": sm, "MODE": m}) for w, sm in ((100, "64"), (100, "48"),
                                                                   (256, "64"), (256, "32"),

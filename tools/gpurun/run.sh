@@ -45,6 +45,24 @@ for step in "$@"; do
     full)   timeout 2400 python -m pytest tests/test_gpu_fullsize.py tests/test_gpu_halo_grad.py tests/test_gpu_async.py -q -x -s -p no:cacheprovider > ${O}_full.log 2>&1; echo "rc=$?" >> ${O}_full.log ;;
     async_roof) nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -o tools/gather_async tools/gather_async.cu \
               && timeout 900 tools/gather_async > ${O}_async_roof.jsonl 2> ${O}_async_roof.err ;;
+    sanitize) CS=/usr/local/cuda/bin/compute-sanitizer
+            for tool in memcheck racecheck synccheck initcheck; do
+              echo "== $tool smoke" >> ${O}_sanitize.log
+              timeout 900 $CS --tool $tool --print-limit 20 python -c "import __graft_entry__ as g; g.smoke()" >> ${O}_sanitize.log 2>&1
+              echo "rc=$?" >> ${O}_sanitize.log
+            done
+            echo "== memcheck cora loopback M=2 (bench)" >> ${O}_sanitize.log
+            timeout 1200 $CS --tool memcheck --print-limit 20 python bench.py --config cora --loopback 2 --steps 2 --warmup 1 --no-e2e --no-ncu >> ${O}_sanitize.log 2>&1
+            echo "rc=$?" >> ${O}_sanitize.log
+            echo "== racecheck cora loopback M=2 (bench)" >> ${O}_sanitize.log
+            timeout 1800 $CS --tool racecheck --print-limit 20 python bench.py --config cora --loopback 2 --steps 1 --warmup 1 --no-e2e --no-ncu >> ${O}_sanitize.log 2>&1
+            echo "rc=$?" >> ${O}_sanitize.log
+            echo "== memcheck peer transport 2 processes" >> ${O}_sanitize.log
+            timeout 1800 $CS --tool memcheck --target-processes all --print-limit 20 python -m pytest tests/test_gpu_peer.py -q -x -k "M2_N1_sgd" -p no:cacheprovider >> ${O}_sanitize.log 2>&1
+            echo "rc=$?" >> ${O}_sanitize.log
+            echo "== memcheck SpMM kernels (lean, tiled, slabs)" >> ${O}_sanitize.log
+            timeout 1800 $CS --tool memcheck --target-processes all --print-limit 20 python -m pytest tests/test_gpu_spmm_variants.py -q -x -k "w48-MM_N1-MODE or w100-MM_N1-MODE or w64-MM_N2 or w256-SMAX64-MODE0" -p no:cacheprovider >> ${O}_sanitize.log 2>&1
+            echo "rc=$?" >> ${O}_sanitize.log ;;
     *)      echo "unknown step $step" >> ${O}_errors.log ;;
   esac
 done

@@ -14,6 +14,7 @@ Two deployments:
   * LoopbackGroup: M partitions in one process on one GPU, stores linked so a push
     writes the peers' back buffers directly (used by the single-GPU tests).
 """
+import contextlib
 from dataclasses import dataclass
 
 import numpy as np
@@ -21,6 +22,14 @@ import torch
 
 from . import capi as D
 from .dist import Schedule
+
+
+def _nvtx(name):
+    """NVTX range around a phase of the epoch (visible to nsys/ncu timelines; a no-op
+    without a profiler attached)."""
+    if torch.cuda.is_available():
+        return torch.cuda.nvtx.range(name)
+    return contextlib.nullcontext()
 
 
 @dataclass
@@ -274,16 +283,23 @@ class DigestWorker:
 
     def epoch(self, r, stream=None):
         """One full DIGEST epoch r (1-based) for a single worker (NCCL deployment)."""
-        if self.cfg.fresh:
-            self.forward_fresh(r, stream)
-        else:
-            sched = Schedule(self.cfg.sync_interval)
-            if sched.pull(r):
-                self.pull(r, stream)
-            self.forward(r, sched.push(r), stream)
-        self.loss_and_backward(stream)
-        self.allreduce(stream)
-        self.update(stream)
+        with _nvtx(f"epoch {r}"):
+            if self.cfg.fresh:
+                with _nvtx("forward (fresh)"):
+                    self.forward_fresh(r, stream)
+            else:
+                sched = Schedule(self.cfg.sync_interval)
+                if sched.pull(r):
+                    with _nvtx("pull"):
+                        self.pull(r, stream)
+                with _nvtx("forward + push" if sched.push(r) else "forward"):
+                    self.forward(r, sched.push(r), stream)
+            with _nvtx("loss + backward"):
+                self.loss_and_backward(stream)
+            with _nvtx("AGG"):
+                self.allreduce(stream)
+            with _nvtx("update"):
+                self.update(stream)
 
     def local_epoch(self, r, stream=None):
         """One DIGEST-A local epoch r (no AGG inside; the PS mixes afterwards):

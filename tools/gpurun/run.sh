@@ -63,6 +63,10 @@ for step in "$@"; do
             echo "== memcheck SpMM kernels (lean, tiled, slabs)" >> ${O}_sanitize.log
             timeout 1800 $CS --tool memcheck --target-processes all --print-limit 20 python -m pytest tests/test_gpu_spmm_variants.py -q -x -k "w48-MM_N1-MODE or w100-MM_N1-MODE or w64-MM_N2 or w256-SMAX64-MODE0" -p no:cacheprovider >> ${O}_sanitize.log 2>&1
             echo "rc=$?" >> ${O}_sanitize.log ;;
+    timeline) timeout 900 python tools/timeline.py --config products --parts 8 --epochs 3 --sync-interval 1 \
+                --out ${O}_timeline_products8.json > ${O}_timeline.log 2>&1
+              timeout 900 python tools/timeline.py --config reddit --parts 4 --epochs 3 --sync-interval 1 \
+                --out ${O}_timeline_reddit4.json >> ${O}_timeline.log 2>&1 ;;
     *)      echo "unknown step $step" >> ${O}_errors.log ;;
   esac
 done

@@ -182,8 +182,12 @@ k_gemm_tf32x3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
           tc::tc_fence_after();
           const uint32_t a = tc::smem_u32(stA(s)), al = tc::smem_u32(stAl(s));
           const uint32_t bh = tc::smem_u32(stBh(s)), bl = tc::smem_u32(stBl(s));
+          // K tail: the last k-block issues only the 8-wide MMA steps that hold real K
+          // (TMA zero-fills the rest; K=100 runs 13 of 16 steps instead of all 16)
+          const int kk = (K - kb * kBK) >= kBK ? kBK / 8 : (K - kb * kBK + 7) / 8;
 #pragma unroll
           for (int k = 0; k < kBK / 8; ++k) {
+            if (k >= kk) break;
             const uint32_t off = k * 32;  // 8 tf32 = 32 bytes along K inside the 128B atom
             const uint64_t dA = tc::smem_desc_sw128(a + off, 16, 1024);
             const uint64_t dAl = tc::smem_desc_sw128(al + off, 16, 1024);

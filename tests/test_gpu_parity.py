@@ -324,7 +324,8 @@ def test_cuda_graph_epoch_replay_matches_eager():
 
 @pytest.mark.parametrize("M,N,K", [(1000, 256, 100), (777, 48, 256), (4096, 16, 1436),
                                    (129, 8, 16), (3000, 256, 256), (5000, 8, 16), (300, 128, 604),
-                                   (2049, 64, 500), (70000, 256, 256)])
+                                   (2049, 64, 500), (70000, 256, 256), (9000, 256, 36),
+                                   (3000, 256, 68), (4100, 48, 4)])
 def test_gemm_parity(M, N, K):
     Dm = D()
     g = torch.Generator().manual_seed(M + N + K)
@@ -336,6 +337,19 @@ def test_gemm_parity(M, N, K):
     assert rel(Cm.cpu().numpy(), ref) <= TOL
     # the 3xTF32 tensor-core path is near-fp32 accurate (plain TF32 would be ~1e-3)
     assert rel(Cm.cpu().numpy(), ref) <= 3e-5, rel(Cm.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("M,N,K", [(1000, 256, 48), (3000, 100, 256), (777, 36, 52)])
+def test_gemm_transposed_b_parity(M, N, K):
+    """DIGEST_GEMM_BT (C = A B^T, B given N x K): the stale halo-gradient term S W^T."""
+    Dm = D()
+    g = torch.Generator().manual_seed(3 * M + N + K)
+    A = torch.rand(M, K, generator=g) * 2 - 1
+    B = torch.rand(N, K, generator=g) * 2 - 1
+    Cm = torch.empty(M, N, device="cuda")
+    Dm.digest_gemm(A.cuda(), B.cuda(), Cm, bt=True)
+    ref = A.double().numpy() @ B.double().numpy().T
+    assert rel(Cm.cpu().numpy(), ref) <= 3e-5
 
 
 # ------------------------------------------------------------------ store (a2, a6)

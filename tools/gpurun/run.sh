@@ -20,7 +20,7 @@ for step in "$@"; do
     smoke)  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > ${O}_smoke.log 2>&1; echo "rc=$?" >> ${O}_smoke.log ;;
     bench)  timeout 900 python bench.py > ${O}_bench.log 2>&1 ;;
     launches) timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none --csv \
-              --log-file ${O}_launches.csv python bench.py --steps 2 --warmup 1 --no-e2e > ${O}_launches.log 2>&1 ;;
+              --log-file ${O}_launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-ncu > ${O}_launches.log 2>&1 ;;
     nsweep) for kv in ${NSWEEP:-"DIGEST_SPMM_N=1" "DIGEST_SPMM_N=5" "DIGEST_SPMM_N=6" "DIGEST_SPMM_N=7" "DIGEST_SPMM_N=8"}; do
               kvs=$(echo $kv | tr ',' ' ')
               echo "== $kvs" >> ${O}_nsweep.log
@@ -67,6 +67,9 @@ for step in "$@"; do
                 --out ${O}_timeline_products8.json > ${O}_timeline.log 2>&1
               timeout 900 python tools/timeline.py --config reddit --parts 4 --epochs 3 --sync-interval 1 \
                 --out ${O}_timeline_reddit4.json >> ${O}_timeline.log 2>&1 ;;
+    l2spmm) for sc in 0.03125 0.0625 0.125 0.25; do
+              timeout 300 python tools/spmm_bench.py --scale $sc --widths 256,100,48 --iters 10 >> ${O}_l2spmm.log 2>&1
+            done ;;
     *)      echo "unknown step $step" >> ${O}_errors.log ;;
   esac
 done

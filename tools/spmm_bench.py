@@ -30,9 +30,15 @@ def main():
     ap.add_argument("--widths", default="256,100,48")
     ap.add_argument("--iters", type=int, default=5)
     ap.add_argument("--mode", type=int, default=0)
+    ap.add_argument("--scale", type=float, default=1.0,
+                    help="nodes and edges of the config scaled by this factor (e.g. an "
+                         "L2-resident footprint)")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     cfg = get_config(a.config)
+    if a.scale != 1.0:
+        from synth.configs import scaled
+        cfg = scaled(cfg, a.scale)
     ip, ix = make_graph(cfg)
     part_of = make_block_parts(cfg, a.parts)
     p = Partition(torch.as_tensor(ip).cuda(), torch.as_tensor(ix).cuda(),
@@ -56,7 +62,7 @@ def main():
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / max(a.iters, 1)
         alg = nnz * (8 + 4 * w) + rows * (4 * w + 8)
-        print(json.dumps({"config": a.config, "parts": a.parts, "mode": a.mode, "width": w,
+        print(json.dumps({"config": a.config, "scale": a.scale, "parts": a.parts, "mode": a.mode, "width": w,
                           "ms": round(ms, 3), "gteps": round(nnz / ms / 1e6, 2),
                           "edge_gather_gbs": round(alg / ms / 1e6, 1),
                           "launches_per_product": lpp, "nnz": nnz, "rows": rows,

@@ -490,137 +490,6 @@ __global__ void __launch_bounds__(256, MB) k_spmm_n(SpmmArgs a, const char* __re
   }
 }
 
-// ---------------------------------------------------------------------------------------
-// Row-pipelined lean kernel (k_spmm_p).  Measured (profiles/r2_spmm_l2_resident_scaling):
-// the lean kernel runs at the same ~43 G nonzeros/s (w=48) whether the sources fit L2
-// or not, i.e. at about half the L2-resident gather roof (tools/gather_roof.cu) -- its
-// warps have no gathers in flight between rows (row_ptr -> (col, val) -> gather chain,
-// cross-group reduction, epilogue).  Here a warp's rows are one stream of ITEMS (STEP
-// = EG*UNR consecutive edges of one row; a row of length L is ceil(L/STEP) items, an
-// empty row one item of zeros) and the loop is software-pipelined by one item: item k+1's
-// gathers are issued (into the second of two register buffers) before item k's FMAs, so
-// a row's reduction and epilogue run while the next row's first gathers are in flight.
-// The producer's (col, val) chunk and the next row's bounds are loaded one item ahead.
-// Offsets are 32-bit (launch_p checks csr_len and n_rows).
-template <int LC, int VPL, int UNR>
-struct PItem {
-  float4 t[UNR][VPL];
-  float x[UNR];
-  int32_t row;
-  bool last, valid;
-};
-
-template <int LC, int VPL, int UNR, bool TWO, bool RAG, int MB>
-__global__ void __launch_bounds__(256, MB) k_spmm_p(SpmmArgs a, const char* __restrict__ x0,
-                                                    const char* __restrict__ x1m,
-                                                    uint32_t split, uint32_t rb_half) {
-  constexpr int EG = 32 / LC;
-  constexpr int STEP = EG * UNR;
-  static_assert(32 % STEP == 0, "an item never straddles a 32-edge chunk");
-  const int lane = threadIdx.x & 31;
-  const int cl = lane % LC;
-  const int g = lane / LC;
-  const int w4 = a.width >> 2;
-  const int32_t n_rows = (int32_t)a.n_rows;
-  const int32_t nwarps = (int32_t)(((int64_t)gridDim.x * blockDim.x) >> 5);
-  const uint64_t pol_s = policy_evict_first();
-
-  auto bounds = [&](int32_t r, int32_t& b, int32_t& e) {
-    b = e = 0;
-    if (r < n_rows) {
-      b = (int32_t)a.row_ptr[r];
-      e = a.in_len ? b + a.in_len[r] : (int32_t)a.row_ptr[r + 1];
-    }
-  };
-  // producer cursor: row prow, next item at ppos, row end pend; chunk [cbase, cbase+32)
-  int32_t prow = (int32_t)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  int32_t ppos, pend, nbeg, nend, cbase;
-  int32_t cc = 0;
-  float cv = 0.f;
-  auto load_chunk = [&](int32_t base, int32_t end) {
-    cbase = base;
-    cc = 0;
-    cv = 0.f;
-    if (base + lane < end) {
-      cc = ld_stream_i(a.col + base + lane, pol_s);
-      cv = ld_stream_f(a.val + base + lane, pol_s);
-    }
-  };
-  bounds(prow, ppos, pend);
-  bounds(prow + nwarps, nbeg, nend);
-  load_chunk(ppos, pend);
-
-  auto produce = [&](PItem<LC, VPL, UNR>& it) {
-    it.valid = prow < n_rows;
-    if (!it.valid) return;
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      const int j = (ppos - cbase) + u * EG + g;   // < 32: items never straddle chunks
-      const uint32_t cr = (uint32_t)__shfl_sync(0xffffffffu, cc, j);
-      it.x[u] = __shfl_sync(0xffffffffu, cv, j);   // 0 past the row's end
-      const char* bs = x0;
-      if (TWO) bs = (cr & 0x7fffffffu) >= split ? x1m : x0;
-      const float4* p = reinterpret_cast<const float4*>(bs + (uint64_t)(cr << 1) * rb_half);
-#pragma unroll
-      for (int q = 0; q < VPL; ++q) {
-        const int idx = cl + q * LC;
-        it.t[u][q] = __ldg(p + (RAG && q == VPL - 1 ? min(idx, w4 - 1) : idx));
-      }
-    }
-    it.row = prow;
-    ppos += STEP;
-    it.last = ppos >= pend;
-    if (it.last) {   // next row: bounds prefetched, its first chunk loads now (used next item)
-      prow += nwarps;
-      ppos = nbeg;
-      pend = nend;
-      bounds(prow + nwarps, nbeg, nend);
-      load_chunk(ppos, pend);
-    } else if (ppos >= cbase + 32) {
-      load_chunk(cbase + 32, pend);
-    }
-  };
-
-  float4 acc[VPL];
-#pragma unroll
-  for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-  auto consume = [&](const PItem<LC, VPL, UNR>& it) {
-#pragma unroll
-    for (int u = 0; u < UNR; ++u)
-#pragma unroll
-      for (int q = 0; q < VPL; ++q) {
-        acc[q].x = fmaf(it.x[u], it.t[u][q].x, acc[q].x);
-        acc[q].y = fmaf(it.x[u], it.t[u][q].y, acc[q].y);
-        acc[q].z = fmaf(it.x[u], it.t[u][q].z, acc[q].z);
-        acc[q].w = fmaf(it.x[u], it.t[u][q].w, acc[q].w);
-      }
-    if (it.last) {
-#pragma unroll
-      for (int off = LC; off < 32; off <<= 1)
-#pragma unroll
-        for (int q = 0; q < VPL; ++q) {
-          acc[q].x += __shfl_down_sync(0xffffffffu, acc[q].x, off);
-          acc[q].y += __shfl_down_sync(0xffffffffu, acc[q].y, off);
-          acc[q].z += __shfl_down_sync(0xffffffffu, acc[q].z, off);
-          acc[q].w += __shfl_down_sync(0xffffffffu, acc[q].w, off);
-        }
-      spmm_row_epilogue<LC, VPL>(a, it.row, lane, cl, g, w4, acc);
-#pragma unroll
-      for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-  };
-
-  PItem<LC, VPL, UNR> A, B;
-  produce(A);
-  while (A.valid) {
-    produce(B);
-    consume(A);
-    if (!B.valid) break;
-    produce(A);
-    consume(B);
-  }
-}
-
 // Single-source product through TMA row gathers (tile::gather4), experimental
 // (DIGEST_SPMM_TMA=1; measured 1.45-1.6x SLOWER than the load-based kernels at w=48/100,
 // products M=1 and 8 parts -- profiles/r1_spmm_variant_sweep.log -- so it is off).  Warp per row as above, but the 32 gathered rows of a (col, val)
@@ -953,37 +822,6 @@ int narrow_variant() {
   return v;
 }
 
-// Row-pipelined kernel launch (k_spmm_p): persistent grid of the resident CTAs.
-template <int LC, int VPL, int UNR, bool RAG, int MB>
-digest_status launch_p(const SpmmArgs& a, cudaStream_t s) {
-  const double W = a.full_width > 0 ? a.full_width : a.width;
-  const double frac = a.width / W;
-  const double bytes = frac * ((double)a.nnz * (8.0 + 4.0 * W) + (double)a.n_rows * (4.0 * W + 8.0));
-  const double flops = 2.0 * (double)a.nnz * a.width;
-  const bool two = !(a.in_len != nullptr || a.X1 == nullptr || a.split >= INT32_MAX);
-  const char* x0 = reinterpret_cast<const char*>(a.X0);
-  const char* x1m = two ? reinterpret_cast<const char*>(a.X1) - a.split * a.ld1 * 4 : x0;
-  const uint32_t rb_half = (uint32_t)(a.ld0 * 2);
-  int64_t blocks = ceil_div(a.n_rows, 8);
-  if (two) {
-    static const int64_t cap = resident_ctas(k_spmm_p<LC, VPL, UNR, true, RAG, MB>);
-    if (blocks > cap) blocks = cap;
-    DG_LAUNCH_TAG(DIGEST_PROF_SPMM, (int)W, s, bytes, flops, (k_spmm_p<LC, VPL, UNR, true, RAG, MB>),
-                  (unsigned)blocks, 256, 0, a, x0, x1m, (uint32_t)a.split, rb_half);
-  } else {
-    static const int64_t cap = resident_ctas(k_spmm_p<LC, VPL, UNR, false, RAG, MB>);
-    if (blocks > cap) blocks = cap;
-    DG_LAUNCH_TAG(DIGEST_PROF_SPMM, (int)W, s, bytes, flops, (k_spmm_p<LC, VPL, UNR, false, RAG, MB>),
-                  (unsigned)blocks, 256, 0, a, x0, x1m, (uint32_t)INT32_MAX, rb_half);
-  }
-  return DIGEST_OK;
-}
-
-// 32-bit offsets of the row-pipelined kernel
-bool pipelined_ok(const SpmmArgs& a) {
-  return a.csr_len > 0 && a.csr_len < INT32_MAX - 64 && a.n_rows < INT32_MAX / 2;
-}
-
 // The lean kernel applies when the two sources share one row stride and every offset
 // fits 32 bits (source rows < 2^31, row bytes < 2^32).
 bool narrow_ok(const SpmmArgs& a) {
@@ -997,23 +835,6 @@ bool narrow_ok(const SpmmArgs& a) {
 digest_status launch_narrow(const SpmmArgs& a, cudaStream_t s) {
   const int w4 = a.width / 4;
   const int v = narrow_variant();
-  if (v >= 4 && v <= 6 && pipelined_ok(a)) {   // row-pipelined experiments
-    if (w4 == 12) {
-      if (v == 5) return launch_p<4, 3, 1, false, 4>(a, s);
-      if (v == 6) return launch_p<4, 3, 2, false, 3>(a, s);
-      return launch_p<4, 3, 2, false, 2>(a, s);
-    }
-    if (w4 == 16) {
-      if (v == 5) return launch_p<4, 4, 1, false, 4>(a, s);
-      if (v == 6) return launch_p<8, 2, 2, false, 3>(a, s);
-      return launch_p<4, 4, 2, false, 2>(a, s);
-    }
-    if (w4 <= 11) return launch_p<4, 3, 2, true, 2>(a, s);
-    if (w4 <= 15) return launch_p<4, 4, 2, true, 2>(a, s);
-    if (v == 5) return launch_p<8, 4, 2, true, 3>(a, s);
-    if (v == 6) return launch_p<8, 4, 4, true, 2>(a, s);
-    return launch_p<8, 4, 2, true, 2>(a, s);
-  }
   // measured, products-shaped partitions (profiles/r2_spmm_sweep.md): w=48 M=1 3.86 ->
   // 2.97 ms, M=8 0.52 -> 0.46 ms; w=100 7.23 -> 6.38 ms
   if (w4 == 12) {
@@ -1179,12 +1000,6 @@ digest_status spmm_one(const SpmmArgs& a, cudaStream_t s) {
       case 4: return launch<16, 4, 4, false>(a, s);
       case 5: return launch<32, 2, 2, false>(a, s);
       case 6: return launch<32, 2, 4, false, 4>(a, s);
-      case 7:
-        if (pipelined_ok(a)) return launch_p<32, 2, 4, false, 2>(a, s);
-        return launch<32, 2, 8>(a, s);
-      case 8:
-        if (pipelined_ok(a)) return launch_p<32, 2, 2, false, 3>(a, s);
-        return launch<32, 2, 8>(a, s);
       // w=256, persistent grid, products M=1: chunk-prefetching <32,2,8> 14.91 ms vs
       // runtime-loop <32,2,4,MB=4> 15.35 ms (profiles/r1_spmm_variant_sweep.log)
       default: return launch<32, 2, 8>(a, s);

@@ -23,10 +23,6 @@ CASES += [(48, {"DIGEST_SPMM_PFH": "1", "DIGEST_SPMM_N": "0"}),
           (48, {"DIGEST_SPMM_GRID": "1", "DIGEST_SPMM_N": "0"})]
 # the lean narrow kernel: every variant, ragged widths, all three products
 CASES += [(w, {"DIGEST_SPMM_N": str(n)}) for w in (48, 64, 100, 128) for n in (1, 2, 3)]
-# the row-pipelined kernel (items of one row, double-buffered gathers)
-CASES += [(w, {"DIGEST_SPMM_N": str(n), "MODE": m}) for w in (48, 64, 100, 20, 52)
-          for n in (4, 5, 6) for m in ("0", "1", "2")]
-CASES += [(256, {"DIGEST_SPMM_V": v, "MODE": m}) for v in ("7", "8") for m in ("0", "1", "2")]
 CASES += [(w, {"DIGEST_SPMM_N": "1", "MODE": m}) for w in (20, 32, 36, 52, 48, 100)
           for m in ("0", "1", "2")]
 # column slabs of the lean kernel (balanced, <= SMAX floats)

@@ -166,6 +166,22 @@ def oracle_sample_epoch_seconds(cfg_name, M, frac, steps, warmup):
     return [t / frac for t in times], sample, round(eff, 2)
 
 
+def full_size_oracle(cfg_name):
+    """The committed timing of ONE unsampled oracle epoch of this workload on a GPU box's
+    host cores (tools/oracle_full_epoch.py), beside the sampled value: it shows how far the
+    linear extrapolation of the sample is off (context, not re-measured in this run)."""
+    p = os.path.join(ROOT, "profiles", "r2_oracle_full_epoch.jsonl")
+    try:
+        for ln in open(p):
+            d = json.loads(ln)
+            if d.get("config") == cfg_name and d.get("frac") == 1.0 and d.get("parts", 1) == 1:
+                return {"epoch_s": d["epoch_s"], "cores_effective": d.get("cores_effective"),
+                        "source": "profiles/r2_oracle_full_epoch.jsonl"}
+    except Exception:   # noqa: BLE001
+        pass
+    return None
+
+
 def cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -335,12 +351,15 @@ def run_ours(a, rank, world, local):
     D.digest_prof_enable(True)
     n0 = D.digest_launch_count()
     barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps + 1)]
+    e0, e1 = ev[0], ev[-1]
     e0.record(stream)
-    for _ in range(a.steps):
+    sched = []
+    for i in range(a.steps):
         r += 1
+        sched.append((r - 1) % n_sync == 0)   # Alg. 1: the epochs that push
         step()
-    e1.record(stream)
+        ev[i + 1].record(stream)
     barrier()
     launches = D.digest_launch_count() - n0 + graph_launches * (a.steps if graph else 0)
     ms = e0.elapsed_time(e1)
@@ -356,6 +375,12 @@ def run_ours(a, rank, world, local):
     D.digest_prof_enable(False)
     ms_max = max_over_ranks(ms)
     step_s = ms_max / 1e3 / a.steps
+    # push and non-push epochs reported separately (rank-local, this rank)
+    per_ep = [ev[i].elapsed_time(ev[i + 1]) for i in range(a.steps)]
+    split = {}
+    for name, want in (("push_epochs", True), ("other_epochs", False)):
+        xs = [t for t, p in zip(per_ep, sched) if p == want]
+        split[name] = {"n": len(xs), "mean_ms": float(np.mean(xs)) if xs else None}
 
     # ---- e2e: same epochs through the public API, every step's inputs copied from pinned
     # host memory inside the timed region.  Input pipeline as a data loader would run it:
@@ -504,7 +529,8 @@ def run_ours(a, rank, world, local):
     if rank == 0 and world == 1 and not loop:   # the oracle baseline is timed at N=1 only
         per, sample, eff = oracle_sample_epoch_seconds(a.config, M, a.sample_frac or 0.1, 1, 1)
         cpu = {"value": float(np.mean(per)), "unit": "s", "cores": eff,
-               "cores_available": cores(), "kind": "oracle", "sample": sample}
+               "cores_available": cores(), "kind": "oracle", "sample": sample,
+               "full_size_check": full_size_oracle(a.config)}
     if rank == 0:
         line = {
             "metric": METRIC, "value": step_s, "unit": "s", "n_gpus": world, "steps": a.steps,
@@ -527,6 +553,7 @@ def run_ours(a, rank, world, local):
             "gpu_launches": int(launches),
             "clocks": clocks,
             "spmm_gteps_rank0": gteps,
+            "epoch_ms_by_schedule_rank0": split,
             "kernel_ms_per_step": {k: v["ms"] / a.steps for k, v in prof.items()},
             # per (class, tag): spmm:<width>, gemm:1KKKKNNN forward-type, 2MMMMNNN weight grad,
             # 3KKKKNNN CTA-pair forward-type

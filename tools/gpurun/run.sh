@@ -70,6 +70,28 @@ for step in "$@"; do
     l2spmm) for sc in 0.03125 0.0625 0.125 0.25; do
               timeout 300 python tools/spmm_bench.py --scale $sc --widths 256,100,48 --iters 10 >> ${O}_l2spmm.log 2>&1
             done ;;
+    matrix) # every config at its M (loopback = all M parts on this GPU)
+            for spec in "products:2:async" "products:4:async" "products:8:async" \
+                        "reddit:1:sync" "reddit:1:async" "reddit:2:sync" "reddit:2:async" \
+                        "reddit:4:sync" "reddit:4:async" "reddit:8:sync" "reddit:8:async" \
+                        "arxiv:4:sync" "arxiv:8:sync" "flickr:2:sync" "flickr:4:sync" "cora:2:sync"; do
+              IFS=: read cfg m mode <<< "$spec"
+              if [ "$m" = "1" ]; then lb=""; else lb="--loopback $m"; fi
+              echo "== $cfg M=$m $mode" >> ${O}_matrix.log
+              timeout 900 python bench.py --config $cfg $lb --mode $mode >> ${O}_matrix.jsonl 2>> ${O}_matrix.log
+            done
+            for spec in "products:8:0" "reddit:8:0" "reddit:1:0"; do
+              IFS=: read cfg m rk <<< "$spec"
+              timeout 900 $NCU --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_sector_hit_rate.pct \
+                --kernel-name regex:k_spmm --clock-control none --csv --log-file ${O}_matrix_ncu_${cfg}${m}.csv \
+                python tools/spmm_bench.py --config $cfg --parts $m --rank $rk --iters 1 \
+                --widths $([ $cfg = reddit ] && echo 256,48 || echo 256,100,48) >> ${O}_matrix.log 2>&1
+            done ;;
+    oracles) for spec in "cora:2:200:1" "cora:2:200:0" "flickr:2:1:0" "flickr:4:1:0" "arxiv:4:1:0" "arxiv:8:1:0" "reddit:1:1:0"; do
+              IFS=: read cfg m ep th <<< "$spec"
+              timeout 1500 python tools/oracle_full_epoch.py --config $cfg --parts $m --epochs $ep --threads $th >> ${O}_oracles.jsonl 2>> ${O}_oracles.log
+            done
+            grep -m1 "model name" /proc/cpuinfo >> ${O}_oracles.log ;;
     *)      echo "unknown step $step" >> ${O}_errors.log ;;
   esac
 done

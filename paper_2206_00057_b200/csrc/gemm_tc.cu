@@ -11,7 +11,9 @@
 //   warp 0      TMA producer: A tile (128 x 32) + B_hi/B_lo tiles (BN x 32), SW128
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (12 MMAs / k-block)
 //   warps 2-5   split workers: A -> (A_hi in place, A_lo) in shared memory
-//   warps 6-9   epilogue: tcgen05.ld -> ReLU -> global stores (double-buffered TMEM)
+//   warps 6-13  epilogue: tcgen05.ld -> ReLU -> global stores (double-buffered TMEM);
+//               two warps per TMEM lane quarter, each draining half of the tile's columns
+//               (the small-K shapes are bound by the epilogue, not the tensor pipe)
 // B (the weight, <= 256 x 1436) is split and transposed to K-major once per call
 // by a small prep kernel into a library-owned workspace.
 #include <cudaTypedefs.h>
@@ -79,7 +81,7 @@ bool make_tmap_rows_fwd(CUtensorMap* m, const void* base, uint64_t inner, uint64
 
 namespace {
 
-constexpr int kBM = 128, kBK = 32, kThreads = 320;
+constexpr int kBM = 128, kBK = 32, kEpiWarps = 8, kThreads = (6 + kEpiWarps) * 32;
 
 constexpr uint32_t pow2_cols(uint32_t c) {
   return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512;
@@ -93,7 +95,7 @@ struct Cfg {
   static constexpr uint32_t B_BYTES = BN * kBK * 4;
   static constexpr uint32_t STAGE = 2 * A_BYTES + 2 * B_BYTES;
   static constexpr int STAGES = (200 * 1024 / STAGE) > 4 ? 4 : (200 * 1024 / STAGE);
-  static constexpr uint32_t EPI = 4 * 4096;                 // per-warp epilogue staging
+  static constexpr uint32_t EPI = kEpiWarps * 4096;         // per-warp epilogue staging
   static constexpr uint32_t SMEM = STAGES * STAGE + EPI + 1024 + 256;
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
   static_assert(B_BYTES % 1024 == 0, "1024-byte aligned stages (SW128 atoms)");
@@ -132,7 +134,7 @@ k_gemm_tf32x3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     }
     for (int a = 0; a < 2; ++a) {
       tc::mbar_init(&tfull[a], 1);
-      tc::mbar_init(&tempty[a], 128);
+      tc::mbar_init(&tempty[a], kEpiWarps * 32);
     }
     tc::fence_mbar_init();
     tc::tma_prefetch(&tmA);
@@ -228,18 +230,22 @@ k_gemm_tf32x3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         if (++s == S) { s = 0; ph ^= 1; }
       }
     }
-  } else {  // ---------------- epilogue (128 threads)
+  } else {  // ---------------- epilogue (256 threads: 2 warps per TMEM lane quarter)
     const int q = warp & 3;   // TMEM lane quarter this warp may access
+    const int half = (warp - 6) >> 2;
+    constexpr int kSplit = ((BN + 1) / 2 + 31) / 32 * 32;
+    const int c_beg = half ? kSplit : 0, c_end = half ? BN : (kSplit < BN ? kSplit : BN);
     int acc = 0;
     uint32_t aph = 0;
-    float4* stg = reinterpret_cast<float4*>(epi + q * 4096);
+    float4* stg = reinterpret_cast<float4*>(epi + (warp - 6) * 4096);
     for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {   // n_tiles_n == 1 (BN >= N)
       const int64_t m0 = t * kBM;
       const int64_t tn = t + gridDim.x;
-      epi_prefetch_next<BN>(e, tn < n_tiles ? tn * kBM : -1, threadIdx.x % 128);
+      if (half == 0)
+        epi_prefetch_next<BN>(e, tn < n_tiles ? tn * kBM : -1, threadIdx.x % 128);
       tc::mbar_wait(&tfull[acc], aph);
       tc::tc_fence_after();
-      epi_tile<BN>(e, tmem_base + acc * G::ACC, stg, m0, q, lane);
+      epi_tile<BN>(e, tmem_base + acc * G::ACC, stg, m0, q, lane, c_beg, c_end);
       tc::tc_fence_before();
       tc::mbar_arrive(&tempty[acc]);
       acc ^= 1;

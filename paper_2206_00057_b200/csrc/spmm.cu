@@ -812,7 +812,8 @@ digest_status launch_n(const SpmmArgs& a, cudaStream_t s) {
 
 // DIGEST_SPMM_N (experiment switch): 0 = the round-1 kernels for narrow widths;
 // 1 = default lean kernel; 2 = cross-row pipelined, 32 gathers per group step (fewer
-// warps); 3 = default without the CSR evict_first policy (profiles/r2_spmm_sweep.md).
+// warps); 3 = default without the CSR evict_first policy; 4 = cross-row pipelined at the
+// default's unroll and occupancy (profiles/r2_spmm_variant_sweeps.log).
 int narrow_variant() {
   static int v = -2;
   if (v == -2) {
@@ -839,11 +840,13 @@ digest_status launch_narrow(const SpmmArgs& a, cudaStream_t s) {
   // 2.97 ms, M=8 0.52 -> 0.46 ms; w=100 7.23 -> 6.38 ms
   if (w4 == 12) {
     if (v == 2) return launch_n<4, 3, 4, false, 3, true, true>(a, s);
+    if (v == 4) return launch_n<4, 3, 2, false, 4, true, true>(a, s);
     if (v == 3) return launch_n<4, 3, 2, false, 4>(a, s);
     return launch_n<4, 3, 2, false, 4, false, true>(a, s);
   }
   if (w4 == 16) {
     if (v == 2) return launch_n<8, 2, 4, false, 3, true, true>(a, s);
+    if (v == 4) return launch_n<4, 4, 2, false, 4, true, true>(a, s);
     if (v == 3) return launch_n<4, 4, 2, false, 4>(a, s);
     return launch_n<4, 4, 2, false, 4, false, true>(a, s);
   }
@@ -852,7 +855,7 @@ digest_status launch_narrow(const SpmmArgs& a, cudaStream_t s) {
   if (w4 <= 11) return launch_n<4, 3, 2, true, 4, false, true>(a, s);
   if (w4 <= 15) return launch_n<4, 4, 2, true, 4, false, true>(a, s);
   // w = 68..128 (products d0 = 100: 25 float4 on 8 lanes x 4, ragged)
-  if (v == 2) return launch_n<8, 4, 2, true, 3, true, true>(a, s);
+  if (v == 2 || v == 4) return launch_n<8, 4, 2, true, 3, true, true>(a, s);
   if (v == 3) return launch_n<8, 4, 2, true, 3>(a, s);
   return launch_n<8, 4, 2, true, 3, false, true>(a, s);
 }

@@ -22,7 +22,8 @@ CASES = [(48, {"DIGEST_SPMM_V12": str(v), "DIGEST_SPMM_N": "0"}) for v in range(
 CASES += [(48, {"DIGEST_SPMM_PFH": "1", "DIGEST_SPMM_N": "0"}),
           (48, {"DIGEST_SPMM_GRID": "1", "DIGEST_SPMM_N": "0"})]
 # the lean narrow kernel: every variant, ragged widths, all three products
-CASES += [(w, {"DIGEST_SPMM_N": str(n)}) for w in (48, 64, 100, 128) for n in (1, 2, 3)]
+CASES += [(w, {"DIGEST_SPMM_N": str(n), "MODE": m}) for w in (48, 64, 100, 128) for n in (1, 2, 3, 4)
+          for m in ("0", "1", "2")]
 CASES += [(w, {"DIGEST_SPMM_N": "1", "MODE": m}) for w in (20, 32, 36, 52, 48, 100)
           for m in ("0", "1", "2")]
 # column slabs of the lean kernel (balanced, <= SMAX floats)

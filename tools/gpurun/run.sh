@@ -92,6 +92,13 @@ for step in "$@"; do
               timeout 1500 python tools/oracle_full_epoch.py --config $cfg --parts $m --epochs $ep --threads $th >> ${O}_oracles.jsonl 2>> ${O}_oracles.log
             done
             grep -m1 "model name" /proc/cpuinfo >> ${O}_oracles.log ;;
+    gemm)   timeout 900 python tools/gemm_bench.py --iters 10 > ${O}_gemm.log 2>&1 ;;
+    ncudense) timeout 1200 $NCU --set full --import-source on --clock-control none \
+                -k regex:"k_gemm|k_wgrad_bf16" -c ${NCUC:-14} -o ${O}_ncu_dense \
+                python tools/gemm_bench.py --iters 1 --shapes ${NCUSHAPES:-256x48,100x256} > ${O}_ncudense.log 2>&1
+              $NCU -i ${O}_ncu_dense.ncu-rep --page raw --csv > ${O}_ncu_dense_raw.csv 2>> ${O}_ncudense.log
+              $NCU -i ${O}_ncu_dense.ncu-rep --page details --csv > ${O}_ncu_dense_details.csv 2>> ${O}_ncudense.log
+              rm -f ${O}_ncu_dense.ncu-rep ;;
     *)      echo "unknown step $step" >> ${O}_errors.log ;;
   esac
 done

@@ -555,6 +555,8 @@ def run_ours(a, rank, world, local):
             "spmm_gteps_rank0": gteps,
             "epoch_ms_by_schedule_rank0": split,
             "kernel_ms_per_step": {k: v["ms"] / a.steps for k, v in prof.items()},
+            # algorithmic flops (2 M N K per GEMM, 2 w per SpMM nonzero, counted once)
+            "kernel_gflop_per_step": {k: v["flops"] / a.steps / 1e9 for k, v in prof.items()},
             # per (class, tag): spmm:<width>, gemm:1KKKKNNN forward-type, 2MMMMNNN weight grad,
             # 3KKKKNNN CTA-pair forward-type
             "kernel_detail_ms_per_step": {f"{d['cls']}:{d['tag']}": round(d["ms"] / a.steps, 3)

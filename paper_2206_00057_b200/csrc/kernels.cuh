@@ -35,6 +35,8 @@ struct SpmmArgs {
   int32_t stream_out;  // 1: evict-first (st.global.cs) stores of the output rows
   int64_t x0_rows;     // rows of X0 (0 = unknown); the TMA row-gather kernel needs it
   int64_t csr_len;     // entries of col/val (0 = unknown); bounds the CSR-tile staging
+  const int32_t* order;  // optional: the rows grouped by length within windows (partition-built;
+                         // the grouped narrow kernel processes rows in this order)
 };
 // 1-bit activation masks: bit (col & 31) of word row * ld + (col >> 5).
 __device__ __forceinline__ bool mask_bit(const uint32_t* bits, int64_t ld, int64_t row, int col) {

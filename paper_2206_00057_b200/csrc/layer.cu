@@ -107,6 +107,7 @@ dg::SpmmArgs spmm_full(const digest_part* p, const float* X0, int64_t ld0, const
   a.ldy = ldy;
   a.width = w;
   a.relu = relu;
+  a.order = p->ord_full;
   return a;
 }
 
@@ -115,6 +116,7 @@ dg::SpmmArgs spmm_in(const digest_part* p, const float* X, int64_t ld, float* Y,
   dg::SpmmArgs a = spmm_full(p, X, ld, X, ld, Y, ldy, w, 0);
   a.in_len = p->in_len;
   a.nnz = p->nnz_in;
+  a.order = p->ord_in;
   return a;
 }
 
@@ -124,6 +126,7 @@ dg::SpmmArgs spmm_rh(const digest_part* p, const float* X, int64_t ld, float* Y,
   dg::SpmmArgs a{};
   a.row_ptr = p->rh_ptr;
   a.in_len = nullptr;
+  a.order = p->ord_rh;
   a.col = p->rh_col;
   a.val = p->rh_val;
   a.n_rows = p->n_halo;

@@ -21,4 +21,9 @@ struct digest_part {
   int64_t* rh_ptr = nullptr;     // [n_halo+1]
   int32_t* rh_col = nullptr;     // [rh_nnz]
   float* rh_val = nullptr;       // [rh_nnz]
+  // row orders for the grouped narrow SpMM (internal): rows grouped by length bin within
+  // windows of consecutive rows, for P (full rows), P_in (in_len) and P_out^T (rh rows)
+  int32_t* ord_full = nullptr;   // [n_local]
+  int32_t* ord_in = nullptr;     // [n_local]
+  int32_t* ord_rh = nullptr;     // [n_halo]
 };

@@ -314,8 +314,66 @@ struct Temps {
   }
 };
 
+// Row order of the grouped narrow SpMM (spmm.cu k_spmm_g, one row per edge group of a
+// warp): within every window of kOrdWin consecutive rows, the rows are grouped by length
+// bin (exact below 64 entries, 32-wide bins above) with a shared-memory counting sort,
+// longest bins first, so the rows one warp handles side by side have similar lengths while
+// the window keeps the row sweep's L2 locality.  The order inside a bin is not specified
+// (atomics): each row's sum is still computed by one group in CSR order, so the product
+// does not depend on it.
+constexpr int kOrdWin = 4096, kOrdBins = 128;
+__device__ __forceinline__ int len_bin(int64_t len) {
+  return len < 64 ? (int)len : 64 + (int)min((int64_t)(kOrdBins - 65), (len - 64) >> 5);
+}
+__global__ void k_len_order(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ in_len,
+                            int64_t n, int32_t* __restrict__ ord) {
+  __shared__ unsigned cnt[kOrdBins];
+  const int64_t w0 = (int64_t)blockIdx.x * kOrdWin;
+  const int64_t w1 = min(n, w0 + kOrdWin);
+  for (int b = threadIdx.x; b < kOrdBins; b += blockDim.x) cnt[b] = 0;
+  __syncthreads();
+  for (int64_t r = w0 + threadIdx.x; r < w1; r += blockDim.x)
+    atomicAdd(&cnt[len_bin(in_len ? in_len[r] : row_ptr[r + 1] - row_ptr[r])], 1u);
+  __syncthreads();
+  if (threadIdx.x == 0) {   // exclusive offsets, longest bin first
+    unsigned acc = 0;
+    for (int b = kOrdBins - 1; b >= 0; --b) {
+      const unsigned c = cnt[b];
+      cnt[b] = acc;
+      acc += c;
+    }
+  }
+  __syncthreads();
+  for (int64_t r = w0 + threadIdx.x; r < w1; r += blockDim.x) {
+    const unsigned pos =
+        atomicAdd(&cnt[len_bin(in_len ? in_len[r] : row_ptr[r + 1] - row_ptr[r])], 1u);
+    ord[w0 + pos] = (int32_t)r;
+  }
+}
+
+digest_status build_orders(digest_part* P, cudaStream_t s) {
+  if (P->n_local > 0) {
+    const unsigned g = (unsigned)dg::ceil_div(P->n_local, kOrdWin);
+    DG_TRY(dmalloc(&P->ord_full, P->n_local));
+    DG_TRY(dmalloc(&P->ord_in, P->n_local));
+    DG_LAUNCH(DIGEST_PROF_OTHER, s, 0, 0, k_len_order, g, 256, 0, P->row_ptr,
+              (const int32_t*)nullptr, P->n_local, P->ord_full);
+    DG_LAUNCH(DIGEST_PROF_OTHER, s, 0, 0, k_len_order, g, 256, 0, P->row_ptr,
+              (const int32_t*)P->in_len, P->n_local, P->ord_in);
+  }
+  if (P->n_halo > 0) {
+    DG_TRY(dmalloc(&P->ord_rh, P->n_halo));
+    DG_LAUNCH(DIGEST_PROF_OTHER, s, 0, 0, k_len_order, (unsigned)dg::ceil_div(P->n_halo, kOrdWin),
+              256, 0, P->rh_ptr, (const int32_t*)nullptr, P->n_halo, P->ord_rh);
+  }
+  return DIGEST_OK;
+}
+
 void free_part(digest_part* p) {
   if (!p) return;
+  cudaFree(p->ord_full);
+  cudaFree(p->ord_in);
+  cudaFree(p->ord_rh);
   cudaFree(p->local_ids);
   cudaFree(p->halo_ids);
   cudaFree(p->row_ptr);
@@ -454,6 +512,7 @@ digest_status build(int64_t N, int64_t nnz, const int64_t* indptr, const int32_t
   DG_CUDA(cudaMemcpyAsync(hs, st, sizeof(hs), cudaMemcpyDeviceToHost, s));
   DG_CUDA(cudaStreamSynchronize(s));
   P->nnz_in = (int64_t)hs[0];
+  DG_TRY(build_orders(P, s));
   P->max_row = (int64_t)hs[1];
   P->max_rh_row = (int64_t)hs[2];
 

@@ -490,6 +490,170 @@ __global__ void __launch_bounds__(256, MB) k_spmm_n(SpmmArgs a, const char* __re
   }
 }
 
+// Grouped narrow kernel (k_spmm_g): one ROW per edge group.  The lean kernel spends a
+// warp on one row -- at every row start the row_ptr -> (col, val) -> gather chain runs with
+// no gathers in flight, and the edge groups' partial sums meet in a shuffle tree -- which
+// keeps it at about half of the L2 gather roof.  Here the EG = 32/LC groups
+// of a warp take EG different rows, taken side by side from the partition's length-grouped
+// row order (digest_part::ord_*: rows grouped by length bin within windows of 4096
+// consecutive rows, so the warp's rows have similar lengths and the sweep keeps its L2
+// locality).  Each group walks its own row UNR edges per step; the chain is paid once per EG
+// rows, no cross-group reduction is needed (a group's lanes own disjoint columns), and the
+// (col, val) of the next step are loaded one step ahead (L1-cached: a group reads its row's
+// 128-byte lines over consecutive steps; L2 evict_first as in the lean kernel).
+__device__ __forceinline__ int32_t ld_csr_i(const int32_t* ptr, uint64_t pol) {
+  int32_t r;
+  asm("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(r) : "l"(ptr), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ float ld_csr_f(const float* ptr, uint64_t pol) {
+  float r;
+  asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(ptr), "l"(pol));
+  return r;
+}
+
+// Group epilogue: the LC lanes of a group hold the whole row (float4 columns cl + q*LC).
+template <int LC, int VPL>
+__device__ __forceinline__ void spmm_group_epilogue(const SpmmArgs& a, int64_t row, int lane,
+                                                    int cl, int w4, const float4 (&acc)[VPL]) {
+  uint32_t nib[VPL];
+#pragma unroll
+  for (int q = 0; q < VPL; ++q) nib[q] = 0;
+  if (row >= 0) {
+    float* y = a.Y + row * a.ldy;
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) {
+      const int idx = cl + q * LC;
+      if (idx < w4) {
+        float4 r = acc[q];
+        if (a.relu) {
+          r.x = fmaxf(r.x, 0.f);
+          r.y = fmaxf(r.y, 0.f);
+          r.z = fmaxf(r.z, 0.f);
+          r.w = fmaxf(r.w, 0.f);
+        }
+        if (a.mask) {
+          const float4 mk = ldg4(a.mask + row * a.ldm + 4 * idx);
+          r.x = mk.x > 0.f ? r.x : 0.f;
+          r.y = mk.y > 0.f ? r.y : 0.f;
+          r.z = mk.z > 0.f ? r.z : 0.f;
+          r.w = mk.w > 0.f ? r.w : 0.f;
+        }
+        if (a.mbits) {
+          const uint32_t m = __ldg(a.mbits + row * a.ldmb + (idx >> 3)) >> ((idx & 7) * 4);
+          r.x = (m & 1u) ? r.x : 0.f;
+          r.y = (m & 2u) ? r.y : 0.f;
+          r.z = (m & 4u) ? r.z : 0.f;
+          r.w = (m & 8u) ? r.w : 0.f;
+        }
+        nib[q] = (r.x > 0.f ? 1u : 0u) | (r.y > 0.f ? 2u : 0u) | (r.z > 0.f ? 4u : 0u) |
+                 (r.w > 0.f ? 8u : 0u);
+        if (a.stream_out)
+          __stcs(reinterpret_cast<float4*>(y) + idx, r);
+        else
+          reinterpret_cast<float4*>(y)[idx] = r;
+      }
+    }
+  }
+  if (a.obits) {   // warp-uniform; word k = float4 columns 8k..8k+7, OR over the group's lanes
+    const int nw = (w4 + 7) >> 3;
+    for (int k = 0; k < nw; ++k) {
+      uint32_t c = 0;
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) {
+        const int idx = cl + q * LC;
+        if ((idx >> 3) == k) c |= nib[q] << ((idx & 7) * 4);
+      }
+#pragma unroll
+      for (int off = 1; off < LC; off <<= 1) c |= __shfl_xor_sync(0xffffffffu, c, off);
+      if (cl == 0 && row >= 0) a.obits[row * a.ldob + k] = c;
+    }
+  }
+  (void)lane;
+}
+
+template <int LC, int VPL, int UNR, bool TWO, bool RAG, int MB>
+__global__ void __launch_bounds__(256, MB) k_spmm_g(SpmmArgs a, const char* __restrict__ x0,
+                                                    const char* __restrict__ x1m,
+                                                    uint32_t split, uint32_t rb_half) {
+  constexpr int EG = 32 / LC;
+  const uint64_t pol_s = policy_evict_first();
+  const int lane = threadIdx.x & 31;
+  const int cl = lane % LC;
+  const int g = lane / LC;
+  const int w4 = a.width >> 2;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = warp * EG; base < a.n_rows; base += nwarps * EG) {
+    const int64_t slot = base + g;
+    int64_t row = -1, beg = 0, end = 0;
+    if (slot < a.n_rows) {
+      row = __ldg(a.order + slot);
+      beg = a.row_ptr[row];
+      end = a.in_len ? beg + a.in_len[row] : a.row_ptr[row + 1];
+    }
+    const int len = (int)(end - beg);
+    const int mx = __reduce_max_sync(0xffffffffu, len);
+    float4 acc[VPL];
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    int32_t c[UNR];
+    float v[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      c[u] = 0;
+      v[u] = 0.f;
+      if (u < len) {
+        c[u] = ld_csr_i(a.col + beg + u, pol_s);
+        v[u] = ld_csr_f(a.val + beg + u, pol_s);
+      }
+    }
+    for (int e = 0; e < mx; e += UNR) {
+      // next step's (col, val): in flight while this step's gathers are
+      int32_t cn[UNR];
+      float vn[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        cn[u] = 0;
+        vn[u] = 0.f;
+        if (e + UNR + u < len) {
+          cn[u] = ld_csr_i(a.col + beg + e + UNR + u, pol_s);
+          vn[u] = ld_csr_f(a.val + beg + e + UNR + u, pol_s);
+        }
+      }
+      // past its row's end a group gathers source row 0 (valid) with weight 0: no predicates
+      float4 t[UNR][VPL];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const uint32_t cr = (uint32_t)c[u];
+        const char* bs = x0;
+        if (TWO) bs = (cr & 0x7fffffffu) >= split ? x1m : x0;
+        const float4* p = reinterpret_cast<const float4*>(bs + (uint64_t)(cr << 1) * rb_half);
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) {
+          const int idx = cl + q * LC;
+          t[u][q] = __ldg(p + (RAG && q == VPL - 1 ? min(idx, w4 - 1) : idx));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u)
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) {
+          acc[q].x = fmaf(v[u], t[u][q].x, acc[q].x);
+          acc[q].y = fmaf(v[u], t[u][q].y, acc[q].y);
+          acc[q].z = fmaf(v[u], t[u][q].z, acc[q].z);
+          acc[q].w = fmaf(v[u], t[u][q].w, acc[q].w);
+        }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        c[u] = cn[u];
+        v[u] = vn[u];
+      }
+    }
+    spmm_group_epilogue<LC, VPL>(a, row, lane, cl, w4, acc);
+  }
+}
+
 // Single-source product through TMA row gathers (tile::gather4), experimental
 // (DIGEST_SPMM_TMA=1; measured 1.45-1.6x SLOWER than the load-based kernels at w=48/100,
 // products M=1 and 8 parts -- profiles/r1_spmm_variant_sweep.log -- so it is off).  Warp per row as above, but the 32 gathered rows of a (col, val)
@@ -810,6 +974,33 @@ digest_status launch_n(const SpmmArgs& a, cudaStream_t s) {
   return DIGEST_OK;
 }
 
+// Grouped kernel launch (k_spmm_g): persistent grid of the resident CTAs; needs the
+// partition's row order (a.order).
+template <int LC, int VPL, int UNR, bool RAG, int MB>
+digest_status launch_g(const SpmmArgs& a, cudaStream_t s) {
+  const double W = a.full_width > 0 ? a.full_width : a.width;
+  const double frac = a.width / W;
+  const double bytes = frac * ((double)a.nnz * (8.0 + 4.0 * W) + (double)a.n_rows * (4.0 * W + 8.0));
+  const double flops = 2.0 * (double)a.nnz * a.width;
+  const bool two = !(a.in_len != nullptr || a.X1 == nullptr || a.split >= INT32_MAX);
+  const char* x0 = reinterpret_cast<const char*>(a.X0);
+  const char* x1m = two ? reinterpret_cast<const char*>(a.X1) - a.split * a.ld1 * 4 : x0;
+  const uint32_t rb_half = (uint32_t)(a.ld0 * 2);
+  int64_t blocks = ceil_div(a.n_rows, 8 * (32 / LC));
+  if (two) {
+    static const int64_t cap = resident_ctas(k_spmm_g<LC, VPL, UNR, true, RAG, MB>);
+    if (blocks > cap) blocks = cap;
+    DG_LAUNCH_TAG(DIGEST_PROF_SPMM, (int)W, s, bytes, flops, (k_spmm_g<LC, VPL, UNR, true, RAG, MB>),
+                  (unsigned)blocks, 256, 0, a, x0, x1m, (uint32_t)a.split, rb_half);
+  } else {
+    static const int64_t cap = resident_ctas(k_spmm_g<LC, VPL, UNR, false, RAG, MB>);
+    if (blocks > cap) blocks = cap;
+    DG_LAUNCH_TAG(DIGEST_PROF_SPMM, (int)W, s, bytes, flops, (k_spmm_g<LC, VPL, UNR, false, RAG, MB>),
+                  (unsigned)blocks, 256, 0, a, x0, x1m, (uint32_t)INT32_MAX, rb_half);
+  }
+  return DIGEST_OK;
+}
+
 // DIGEST_SPMM_N (experiment switch): 0 = the round-1 kernels for narrow widths;
 // 1 = default lean kernel; 2 = cross-row pipelined, 32 gathers per group step (fewer
 // warps); 3 = default without the CSR evict_first policy; 4 = cross-row pipelined at the
@@ -836,6 +1027,21 @@ bool narrow_ok(const SpmmArgs& a) {
 digest_status launch_narrow(const SpmmArgs& a, cudaStream_t s) {
   const int w4 = a.width / 4;
   const int v = narrow_variant();
+  if (v >= 5 && v <= 7 && a.order) {   // grouped kernel (one row per edge group)
+    if (w4 == 12) {
+      if (v == 6) return launch_g<4, 3, 4, false, 3>(a, s);
+      if (v == 7) return launch_g<2, 6, 2, false, 3>(a, s);
+      return launch_g<4, 3, 2, false, 4>(a, s);
+    }
+    if (w4 == 16) return launch_g<4, 4, 2, false, 4>(a, s);
+    if (w4 == 8) return launch_g<4, 2, 2, false, 4>(a, s);
+    if (w4 <= 7) return launch_g<4, 2, 2, true, 4>(a, s);
+    if (w4 <= 11) return launch_g<4, 3, 2, true, 4>(a, s);
+    if (w4 <= 15) return launch_g<4, 4, 2, true, 4>(a, s);
+    if (v == 6) return launch_g<8, 4, 4, true, 2>(a, s);
+    if (v == 7) return launch_g<4, 7, 2, true, 3>(a, s);
+    return launch_g<8, 4, 2, true, 3>(a, s);
+  }
   // measured, products-shaped partitions (profiles/r2_spmm_sweep.md): w=48 M=1 3.86 ->
   // 2.97 ms, M=8 0.52 -> 0.46 ms; w=100 7.23 -> 6.38 ms
   if (w4 == 12) {

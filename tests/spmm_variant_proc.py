@@ -9,11 +9,11 @@ import numpy as np
 import torch
 
 
-def main(out, width, seed, mode=0):
+def main(out, width, seed, mode=0, nodes=3000):
     torch.cuda.set_device(0)
     from paper_2206_00057_b200.engine import Partition
     from synth import small_config, make_graph, make_random_parts
-    cfg = small_config(num_nodes=3000, nnz=90000, d0=8, hidden=(8,), seed=seed)
+    cfg = small_config(num_nodes=nodes, nnz=30 * nodes, d0=8, hidden=(8,), seed=seed)
     ip, ix = make_graph(cfg)
     part = make_random_parts(cfg.num_nodes, 3, seed)
     p = Partition(torch.as_tensor(ip).cuda(), torch.as_tensor(ix).cuda(),
@@ -31,4 +31,4 @@ def main(out, width, seed, mode=0):
 
 if __name__ == "__main__":
     main(sys.argv[1], int(sys.argv[2]), int(sys.argv[3]),
-         int(sys.argv[4]) if len(sys.argv) > 4 else 0)
+         int(sys.argv[4]) if len(sys.argv) > 4 else 0, int(sys.argv[5]) if len(sys.argv) > 5 else 3000)

@@ -22,10 +22,13 @@ CASES = [(48, {"DIGEST_SPMM_V12": str(v), "DIGEST_SPMM_N": "0"}) for v in range(
 CASES += [(48, {"DIGEST_SPMM_PFH": "1", "DIGEST_SPMM_N": "0"}),
           (48, {"DIGEST_SPMM_GRID": "1", "DIGEST_SPMM_N": "0"})]
 # the lean narrow kernel: every variant, ragged widths, all three products
-CASES += [(w, {"DIGEST_SPMM_N": str(n), "MODE": m}) for w in (48, 64, 100, 128) for n in (1, 2, 3, 4)
+CASES += [(w, {"DIGEST_SPMM_N": str(n), "MODE": m}) for w in (48, 64, 100, 128) for n in (1, 2, 3, 4, 5, 6, 7)
           for m in ("0", "1", "2")]
-CASES += [(w, {"DIGEST_SPMM_N": "1", "MODE": m}) for w in (20, 32, 36, 52, 48, 100)
+CASES += [(w, {"DIGEST_SPMM_N": n, "MODE": m}) for n in ("1", "5") for w in (20, 32, 36, 52, 48, 100)
           for m in ("0", "1", "2")]
+# several 4096-row windows of the partition's length-grouped row order (grouped kernel)
+CASES += [(w, {"DIGEST_SPMM_N": n, "MODE": m, "NODES": "40000"}) for n in ("1", "5")
+          for w in (48, 100) for m in ("0", "1", "2")]
 # column slabs of the lean kernel (balanced, <= SMAX floats)
 CASES += [(w, {"DIGEST_SPMM_SMAX": sm, "MODE": m}) for w, sm in ((100, "64"), (100, "48"),
                                                                   (256, "64"), (256, "32"),
@@ -53,8 +56,9 @@ def test_spmm_variant(width, env, tmp_path):
     out = str(tmp_path / "y.npz")
     env = dict(env)
     mode = int(env.pop("MODE", "0"))
+    nodes = env.pop("NODES", "3000")
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "spmm_variant_proc.py"), out,
-                        str(width), "5", str(mode)], env={**os.environ, **env, "DIGEST_KNOBS": "1", "PYTHONPATH": ROOT},
+                        str(width), "5", str(mode), nodes], env={**os.environ, **env, "DIGEST_KNOBS": "1", "PYTHONPATH": ROOT},
                        capture_output=True, text=True, timeout=280)
     assert r.returncode == 0, r.stderr[-2000:]
     d = np.load(out)

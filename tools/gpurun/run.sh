@@ -27,7 +27,7 @@ for step in "$@"; do
               env DIGEST_KNOBS=1 $kvs timeout 300 python tools/spmm_bench.py --widths ${NW:-256,100,48} --iters 5 >> ${O}_nsweep.log 2>&1
               env DIGEST_KNOBS=1 $kvs timeout 300 python tools/spmm_bench.py --parts 8 --widths ${NW:-256,100,48} --iters 5 >> ${O}_nsweep.log 2>&1
             done ;;
-    variants) timeout 1200 python -m pytest tests/test_gpu_spmm_variants.py -q -x -p no:cacheprovider > ${O}_variants.log 2>&1 ;;
+    variants) timeout 1500 python -m pytest tests/test_gpu_spmm_variants.py -q -x -p no:cacheprovider ${VK:+-k "$VK"} > ${O}_variants.log 2>&1 ;;
     parity) timeout 1800 python -m pytest tests/test_gpu_parity.py -q -x -p no:cacheprovider > ${O}_parity.log 2>&1; echo "rc=$?" >> ${O}_parity.log ;;
     oraclefull) timeout 1500 python tools/oracle_full_epoch.py --frac 1.0 > ${O}_oraclefull.log 2>&1
                 timeout 600 python tools/oracle_full_epoch.py --frac 0.1 >> ${O}_oraclefull.log 2>&1 ;;

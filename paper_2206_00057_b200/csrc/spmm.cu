@@ -575,16 +575,24 @@ __device__ __forceinline__ void spmm_group_epilogue(const SpmmArgs& a, int64_t r
 template <int LC, int VPL, int UNR, bool TWO, bool RAG, int MB>
 __global__ void __launch_bounds__(256, MB) k_spmm_g(SpmmArgs a, const char* __restrict__ x0,
                                                     const char* __restrict__ x1m,
-                                                    uint32_t split, uint32_t rb_half) {
+                                                    uint32_t split, uint32_t rb_half,
+                                                    unsigned long long* __restrict__ ctr) {
   constexpr int EG = 32 / LC;
   const uint64_t pol_s = policy_evict_first();
   const int lane = threadIdx.x & 31;
   const int cl = lane % LC;
   const int g = lane / LC;
   const int w4 = a.width >> 2;
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t base = warp * EG; base < a.n_rows; base += nwarps * EG) {
+  // Batches of EG slots are handed out by an atomic counter (zeroed before the launch): a
+  // warp that drew long rows simply draws fewer batches, so the rows in flight stay one
+  // narrow window and the sweep keeps its L2 locality.  (A static round-robin deal drifts:
+  // the length-grouped order gives some warps systematically longer rows, and the window
+  // spread over several planted blocks -- L2 hit 65% -> 23-36%, measured.)
+  for (;;) {
+    unsigned long long b0 = 0;
+    if (lane == 0) b0 = atomicAdd(ctr, (unsigned long long)EG);
+    const int64_t base = (int64_t)__shfl_sync(0xffffffffu, b0, 0);
+    if (base >= a.n_rows) break;
     const int64_t slot = base + g;
     int64_t row = -1, beg = 0, end = 0;
     if (slot < a.n_rows) {
@@ -976,8 +984,23 @@ digest_status launch_n(const SpmmArgs& a, cudaStream_t s) {
 
 // Grouped kernel launch (k_spmm_g): persistent grid of the resident CTAs; needs the
 // partition's row order (a.order).
+// Work counters of the grouped kernel: a ring of slots, one per launch, zeroed on the
+// launching stream right before it (graph-capturable; launches on different streams in
+// flight at once take different slots).
+unsigned long long* grab_counter(cudaStream_t s) {
+  static unsigned long long* ring = nullptr;
+  static unsigned next = 0;
+  constexpr unsigned kSlots = 64;
+  if (!ring && cudaMalloc(&ring, kSlots * 128) != cudaSuccess) return nullptr;
+  unsigned long long* c = ring + (next++ % kSlots) * 16;   // 128-byte apart
+  if (cudaMemsetAsync(c, 0, sizeof(unsigned long long), s) != cudaSuccess) return nullptr;
+  return c;
+}
+
 template <int LC, int VPL, int UNR, bool RAG, int MB>
 digest_status launch_g(const SpmmArgs& a, cudaStream_t s) {
+  unsigned long long* ctr = grab_counter(s);
+  DG_ARG(ctr, DIGEST_E_CUDA, "SpMM work counter allocation failed");
   const double W = a.full_width > 0 ? a.full_width : a.width;
   const double frac = a.width / W;
   const double bytes = frac * ((double)a.nnz * (8.0 + 4.0 * W) + (double)a.n_rows * (4.0 * W + 8.0));
@@ -991,12 +1014,12 @@ digest_status launch_g(const SpmmArgs& a, cudaStream_t s) {
     static const int64_t cap = resident_ctas(k_spmm_g<LC, VPL, UNR, true, RAG, MB>);
     if (blocks > cap) blocks = cap;
     DG_LAUNCH_TAG(DIGEST_PROF_SPMM, (int)W, s, bytes, flops, (k_spmm_g<LC, VPL, UNR, true, RAG, MB>),
-                  (unsigned)blocks, 256, 0, a, x0, x1m, (uint32_t)a.split, rb_half);
+                  (unsigned)blocks, 256, 0, a, x0, x1m, (uint32_t)a.split, rb_half, ctr);
   } else {
     static const int64_t cap = resident_ctas(k_spmm_g<LC, VPL, UNR, false, RAG, MB>);
     if (blocks > cap) blocks = cap;
     DG_LAUNCH_TAG(DIGEST_PROF_SPMM, (int)W, s, bytes, flops, (k_spmm_g<LC, VPL, UNR, false, RAG, MB>),
-                  (unsigned)blocks, 256, 0, a, x0, x1m, (uint32_t)INT32_MAX, rb_half);
+                  (unsigned)blocks, 256, 0, a, x0, x1m, (uint32_t)INT32_MAX, rb_half, ctr);
   }
   return DIGEST_OK;
 }
@@ -1004,7 +1027,8 @@ digest_status launch_g(const SpmmArgs& a, cudaStream_t s) {
 // DIGEST_SPMM_N (experiment switch): 0 = the round-1 kernels for narrow widths;
 // 1 = default lean kernel; 2 = cross-row pipelined, 32 gathers per group step (fewer
 // warps); 3 = default without the CSR evict_first policy; 4 = cross-row pipelined at the
-// default's unroll and occupancy (profiles/r2_spmm_variant_sweeps.log).
+// default's unroll and occupancy (profiles/r2_spmm_variant_sweeps.log); 5-9 = the grouped
+// kernel (k_spmm_g) at every narrow width with different unroll / lane layouts.
 int narrow_variant() {
   static int v = -2;
   if (v == -2) {
@@ -1027,8 +1051,14 @@ bool narrow_ok(const SpmmArgs& a) {
 digest_status launch_narrow(const SpmmArgs& a, cudaStream_t s) {
   const int w4 = a.width / 4;
   const int v = narrow_variant();
-  if (v >= 5 && v <= 7 && a.order) {   // grouped kernel (one row per edge group)
+  // Default (v == 1): the grouped kernel for w = 68..128 (products d0 = 100: 6.23 -> 4.52
+  // ms at M=1, 0.90 -> 0.85 ms on one 8-part partition), the lean kernel below 68 floats
+  // (w=48: grouped 2.77 vs 2.91 ms at M=1 but 0.57 vs 0.46 ms at M=8;
+  // profiles/r2_spmm_grouped_sweep.log).
+  if (v == 1 && a.order && w4 > 16) return launch_g<8, 4, 4, true, 2>(a, s);
+  if (v >= 5 && v <= 9 && a.order) {   // grouped kernel experiments (one row per edge group)
     if (w4 == 12) {
+      if (v == 9) return launch_g<4, 3, 3, false, 3>(a, s);
       if (v == 6) return launch_g<4, 3, 4, false, 3>(a, s);
       if (v == 7) return launch_g<2, 6, 2, false, 3>(a, s);
       return launch_g<4, 3, 2, false, 4>(a, s);
@@ -1039,7 +1069,8 @@ digest_status launch_narrow(const SpmmArgs& a, cudaStream_t s) {
     if (w4 <= 11) return launch_g<4, 3, 2, true, 4>(a, s);
     if (w4 <= 15) return launch_g<4, 4, 2, true, 4>(a, s);
     if (v == 6) return launch_g<8, 4, 4, true, 2>(a, s);
-    if (v == 7) return launch_g<4, 7, 2, true, 3>(a, s);
+    if (v == 8) return launch_g<8, 4, 3, true, 2>(a, s);
+    if (v == 7 && w4 <= 28) return launch_g<4, 7, 2, true, 3>(a, s);
     return launch_g<8, 4, 2, true, 3>(a, s);
   }
   // measured, products-shaped partitions (profiles/r2_spmm_sweep.md): w=48 M=1 3.86 ->

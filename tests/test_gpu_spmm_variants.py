@@ -22,7 +22,7 @@ CASES = [(48, {"DIGEST_SPMM_V12": str(v), "DIGEST_SPMM_N": "0"}) for v in range(
 CASES += [(48, {"DIGEST_SPMM_PFH": "1", "DIGEST_SPMM_N": "0"}),
           (48, {"DIGEST_SPMM_GRID": "1", "DIGEST_SPMM_N": "0"})]
 # the lean narrow kernel: every variant, ragged widths, all three products
-CASES += [(w, {"DIGEST_SPMM_N": str(n), "MODE": m}) for w in (48, 64, 100, 128) for n in (1, 2, 3, 4, 5, 6, 7)
+CASES += [(w, {"DIGEST_SPMM_N": str(n), "MODE": m}) for w in (48, 64, 100, 128) for n in (1, 2, 3, 4, 5, 6, 7, 8, 9)
           for m in ("0", "1", "2")]
 CASES += [(w, {"DIGEST_SPMM_N": n, "MODE": m}) for n in ("1", "5") for w in (20, 32, 36, 52, 48, 100)
           for m in ("0", "1", "2")]

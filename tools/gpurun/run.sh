@@ -93,6 +93,13 @@ for step in "$@"; do
             done
             grep -m1 "model name" /proc/cpuinfo >> ${O}_oracles.log ;;
     gemm)   timeout 900 python tools/gemm_bench.py --iters 10 > ${O}_gemm.log 2>&1 ;;
+    ncuk)   # one SpMM kernel, full set + source: NCUK_KNOBS (comma list), NCUK_W width, NCUK_NAME tag
+            env DIGEST_KNOBS=1 $(echo ${NCUK_KNOBS} | tr ',' ' ') timeout 900 $NCU --set full --import-source on \
+              --clock-control none -k regex:k_spmm -c 1 -o ${O}_ncu_${NCUK_NAME} \
+              python tools/spmm_bench.py --widths ${NCUK_W:-48} --iters 1 > ${O}_ncuk_${NCUK_NAME}.log 2>&1
+            $NCU -i ${O}_ncu_${NCUK_NAME}.ncu-rep --page details --csv > ${O}_ncu_${NCUK_NAME}_details.csv 2>> ${O}_ncuk_${NCUK_NAME}.log
+            $NCU -i ${O}_ncu_${NCUK_NAME}.ncu-rep --page source --csv > ${O}_ncu_${NCUK_NAME}_source.csv 2>> ${O}_ncuk_${NCUK_NAME}.log
+            gzip -f ${O}_ncu_${NCUK_NAME}_source.csv; rm -f ${O}_ncu_${NCUK_NAME}.ncu-rep ;;
     ncudense) timeout 1200 $NCU --set full --import-source on --clock-control none \
                 -k regex:"k_gemm|k_wgrad_bf16" -c ${NCUC:-14} -o ${O}_ncu_dense \
                 python tools/gemm_bench.py --iters 1 --shapes ${NCUSHAPES:-256x48,100x256} > ${O}_ncudense.log 2>&1

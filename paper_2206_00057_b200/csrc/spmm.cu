@@ -605,6 +605,68 @@ __global__ void __launch_bounds__(256, MB) k_spmm_g(SpmmArgs a, const char* __re
     float4 acc[VPL];
 #pragma unroll
     for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    // A batch from the long tail (rows up to 5k entries; the length bins are 32 wide above
+    // 64) can be far from uniform: side by side its groups would all wait for the longest
+    // row (max / UNR steps).  Then the warp takes the batch's rows one at a time instead,
+    // all groups on one row as in the lean kernel (sum / (EG UNR) steps + one chain per row).
+    const int sum = __reduce_add_sync(0xffffffffu, cl == 0 ? len : 0);
+    if (mx * EG > sum + 64 * EG) {
+      for (int r = 0; r < EG; ++r) {
+        const int64_t rr = __shfl_sync(0xffffffffu, row, r * LC);
+        const int64_t rb = __shfl_sync(0xffffffffu, beg, r * LC);
+        const int64_t re = __shfl_sync(0xffffffffu, end, r * LC);
+        if (rr < 0) continue;   // warp-uniform
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int64_t e0 = rb; e0 < re; e0 += 32) {
+          int32_t cc = 0;
+          float vv = 0.f;
+          if (e0 + lane < re) {
+            cc = ld_csr_i(a.col + e0 + lane, pol_s);
+            vv = ld_csr_f(a.val + e0 + lane, pol_s);
+          }
+          const int cnt = (int)min((int64_t)32, re - e0);
+          for (int j0 = 0; j0 < cnt; j0 += EG * UNR) {   // warp-uniform
+            float4 t[UNR][VPL];
+            float x[UNR];
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+              const int j = j0 + u * EG + g;   // < 32; past cnt: (col 0, val 0)
+              const uint32_t cr = (uint32_t)__shfl_sync(0xffffffffu, cc, j);
+              x[u] = __shfl_sync(0xffffffffu, vv, j);
+              const char* bs = x0;
+              if (TWO) bs = (cr & 0x7fffffffu) >= split ? x1m : x0;
+              const float4* p = reinterpret_cast<const float4*>(bs + (uint64_t)(cr << 1) * rb_half);
+#pragma unroll
+              for (int q = 0; q < VPL; ++q) {
+                const int idx = cl + q * LC;
+                t[u][q] = __ldg(p + (RAG && q == VPL - 1 ? min(idx, w4 - 1) : idx));
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < UNR; ++u)
+#pragma unroll
+              for (int q = 0; q < VPL; ++q) {
+                acc[q].x = fmaf(x[u], t[u][q].x, acc[q].x);
+                acc[q].y = fmaf(x[u], t[u][q].y, acc[q].y);
+                acc[q].z = fmaf(x[u], t[u][q].z, acc[q].z);
+                acc[q].w = fmaf(x[u], t[u][q].w, acc[q].w);
+              }
+          }
+        }
+#pragma unroll
+        for (int off = LC; off < 32; off <<= 1)   // tree over the edge groups
+#pragma unroll
+          for (int q = 0; q < VPL; ++q) {
+            acc[q].x += __shfl_down_sync(0xffffffffu, acc[q].x, off);
+            acc[q].y += __shfl_down_sync(0xffffffffu, acc[q].y, off);
+            acc[q].z += __shfl_down_sync(0xffffffffu, acc[q].z, off);
+            acc[q].w += __shfl_down_sync(0xffffffffu, acc[q].w, off);
+          }
+        spmm_row_epilogue<LC, VPL>(a, rr, lane, cl, g, w4, acc);
+      }
+      continue;
+    }
     int32_t c[UNR];
     float v[UNR];
 #pragma unroll

@@ -1113,11 +1113,15 @@ bool narrow_ok(const SpmmArgs& a) {
 digest_status launch_narrow(const SpmmArgs& a, cudaStream_t s) {
   const int w4 = a.width / 4;
   const int v = narrow_variant();
-  // Default (v == 1): the grouped kernel for w = 68..128 (products d0 = 100: 6.23 -> 4.52
-  // ms at M=1, 0.90 -> 0.85 ms on one 8-part partition), the lean kernel below 68 floats
-  // (w=48: grouped 2.77 vs 2.91 ms at M=1 but 0.57 vs 0.46 ms at M=8;
-  // profiles/r2_spmm_grouped_sweep.log).
+  // Default (v == 1), measured on products-shaped partitions
+  // (profiles/r2_spmm_grouped_sweep.log): the grouped kernel for w = 68..128 (d0 = 100:
+  // M=1 6.23 -> 4.50 ms, one 8-part partition 0.90 -> 0.83 ms) and for w = 48 on products
+  // of >= 1M rows (M=1: 2.96 -> 2.22 ms).  On smaller products (an 8-part partition, 306K
+  // rows) the w=48 grouped kernel loses (0.46 -> 0.55 ms): 8 rows per warp batch leave only
+  // ~11 batches per warp and the last wave's imbalance shows, so the lean kernel stays.
   if (v == 1 && a.order && w4 > 16) return launch_g<8, 4, 4, true, 2>(a, s);
+  if (v == 1 && a.order && w4 == 12 && a.n_rows >= (1 << 20))
+    return launch_g<4, 3, 4, false, 3>(a, s);
   if (v >= 5 && v <= 9 && a.order) {   // grouped kernel experiments (one row per edge group)
     if (w4 == 12) {
       if (v == 9) return launch_g<4, 3, 3, false, 3>(a, s);

@@ -63,6 +63,13 @@ for step in "$@"; do
             echo "== memcheck SpMM kernels (lean, tiled, slabs)" >> ${O}_sanitize.log
             timeout 1800 $CS --tool memcheck --target-processes all --print-limit 20 python -m pytest tests/test_gpu_spmm_variants.py -q -x -k "w48-MM_N1-MODE or w100-MM_N1-MODE or w64-MM_N2 or w256-SMAX64-MODE0" -p no:cacheprovider >> ${O}_sanitize.log 2>&1
             echo "rc=$?" >> ${O}_sanitize.log ;;
+    sanitize2) CS=/usr/local/cuda/bin/compute-sanitizer   # the round-2 grouped SpMM kernel
+            for tool in memcheck racecheck synccheck; do
+              echo "== $tool grouped SpMM (w100 default, w48 N6, multi-window)" >> ${O}_sanitize2.log
+              timeout 1500 $CS --tool $tool --target-processes all --print-limit 20 python -m pytest tests/test_gpu_spmm_variants.py -q -x \
+                -k "w100-MM_N1-MODE0-ODES40000 or w48-MM_N6-MODE0 or w100-MM_N1-MODE2-ODES40000" -p no:cacheprovider >> ${O}_sanitize2.log 2>&1
+              echo "rc=$?" >> ${O}_sanitize2.log
+            done ;;
     timeline) timeout 900 python tools/timeline.py --config products --parts 8 --epochs 3 --sync-interval 1 \
                 --out ${O}_timeline_products8.json > ${O}_timeline.log 2>&1
               timeout 900 python tools/timeline.py --config reddit --parts 4 --epochs 3 --sync-interval 1 \

@@ -316,24 +316,30 @@ struct Temps {
 
 // Row order of the grouped narrow SpMM (spmm.cu k_spmm_g, one row per edge group of a
 // warp): within every window of kOrdWin consecutive rows, the rows are grouped by length
-// bin (exact below 64 entries, 32-wide bins above) with a shared-memory counting sort,
-// longest bins first, so the rows one warp handles side by side have similar lengths while
-// the window keeps the row sweep's L2 locality.  The order inside a bin is not specified
-// (atomics): each row's sum is still computed by one group in CSR order, so the product
-// does not depend on it.
+// bin (exact below 64 entries, 32-wide bins above), longest bin first, ascending row id
+// inside a bin (a stable counting sort: deterministic, so every process that builds the
+// same partition gets the same order -- the kernel's per-row path, and hence its rounding,
+// depends on the batches the order forms).  The rows one warp handles side by side then
+// have similar lengths, and the window keeps the row sweep's L2 locality.
 constexpr int kOrdWin = 4096, kOrdBins = 128;
 __device__ __forceinline__ int len_bin(int64_t len) {
   return len < 64 ? (int)len : 64 + (int)min((int64_t)(kOrdBins - 65), (len - 64) >> 5);
 }
-__global__ void k_len_order(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ in_len,
-                            int64_t n, int32_t* __restrict__ ord) {
+__global__ void __launch_bounds__(256) k_len_order(const int64_t* __restrict__ row_ptr,
+                                                   const int32_t* __restrict__ in_len, int64_t n,
+                                                   int32_t* __restrict__ ord) {
+  __shared__ uint8_t bins[kOrdWin];
   __shared__ unsigned cnt[kOrdBins];
   const int64_t w0 = (int64_t)blockIdx.x * kOrdWin;
-  const int64_t w1 = min(n, w0 + kOrdWin);
+  const int nw = (int)min((int64_t)kOrdWin, n - w0);
   for (int b = threadIdx.x; b < kOrdBins; b += blockDim.x) cnt[b] = 0;
   __syncthreads();
-  for (int64_t r = w0 + threadIdx.x; r < w1; r += blockDim.x)
-    atomicAdd(&cnt[len_bin(in_len ? in_len[r] : row_ptr[r + 1] - row_ptr[r])], 1u);
+  for (int i = threadIdx.x; i < nw; i += blockDim.x) {
+    const int64_t r = w0 + i;
+    const int b = len_bin(in_len ? in_len[r] : row_ptr[r + 1] - row_ptr[r]);
+    bins[i] = (uint8_t)b;
+    atomicAdd(&cnt[b], 1u);
+  }
   __syncthreads();
   if (threadIdx.x == 0) {   // exclusive offsets, longest bin first
     unsigned acc = 0;
@@ -344,10 +350,11 @@ __global__ void k_len_order(const int64_t* __restrict__ row_ptr, const int32_t* 
     }
   }
   __syncthreads();
-  for (int64_t r = w0 + threadIdx.x; r < w1; r += blockDim.x) {
-    const unsigned pos =
-        atomicAdd(&cnt[len_bin(in_len ? in_len[r] : row_ptr[r + 1] - row_ptr[r])], 1u);
-    ord[w0 + pos] = (int32_t)r;
+  if (threadIdx.x < kOrdBins) {   // one thread per bin walks the window in row order
+    const uint8_t b = (uint8_t)threadIdx.x;
+    unsigned pos = cnt[b];
+    for (int i = 0; i < nw; ++i)
+      if (bins[i] == b) ord[w0 + pos++] = (int32_t)(w0 + i);
   }
 }
 

@@ -43,6 +43,9 @@ __device__ __forceinline__ bool mask_bit(const uint32_t* bits, int64_t ld, int64
   return (__ldg(bits + row * ld + (col >> 5)) >> (col & 31)) & 1u;
 }
 digest_status spmm(const SpmmArgs& a, cudaStream_t s);
+// Allocates (once) the work counters of the grouped SpMM; called at partition build, so no
+// allocation happens inside a launch that may be stream-captured.  false on failure.
+bool spmm_counters_init();
 
 // C = A * B (+ optional ReLU) with generic strides:
 //   A(i,k) = A[i*sAi + k*sAk],  B(k,j) = B[k*sBk + j*sBj],  C[i*ldc + j].

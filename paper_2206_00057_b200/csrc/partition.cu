@@ -6,6 +6,7 @@
 // match/ballot ranks.  One-time setup; not on the epoch path.
 #include <vector>
 
+#include "kernels.cuh"
 #include "part_internal.cuh"
 #include "scan.cuh"
 
@@ -359,6 +360,7 @@ __global__ void __launch_bounds__(256) k_len_order(const int64_t* __restrict__ r
 }
 
 digest_status build_orders(digest_part* P, cudaStream_t s) {
+  DG_ARG(dg::spmm_counters_init(), DIGEST_E_NOMEM, "SpMM work counter allocation failed");
   if (P->n_local > 0) {
     const unsigned g = (unsigned)dg::ceil_div(P->n_local, kOrdWin);
     DG_TRY(dmalloc(&P->ord_full, P->n_local));

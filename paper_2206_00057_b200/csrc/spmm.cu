@@ -8,6 +8,9 @@
 // contiguous X_ext).  HBM-bound: ~2 flop per (8 + 4w) bytes per nonzero.
 #include <cudaTypedefs.h>
 
+#include <atomic>
+#include <mutex>
+
 #include "kernels.cuh"
 #include "tc_util.cuh"
 
@@ -1049,12 +1052,17 @@ digest_status launch_n(const SpmmArgs& a, cudaStream_t s) {
 // Work counters of the grouped kernel: a ring of slots, one per launch, zeroed on the
 // launching stream right before it (graph-capturable; launches on different streams in
 // flight at once take different slots).
+// (A slot is reused 64 launches later: safe on one stream, and on several unless more
+// than 64 grouped launches are in flight at once.)  The ring is allocated when a partition
+// is built (spmm_counters_init), never inside a launch that may be stream-captured.
+constexpr unsigned kCtrSlots = 64;
+unsigned long long* g_ctr_ring = nullptr;
+std::once_flag g_ctr_once;
+std::atomic<unsigned> g_ctr_next{0};
+
 unsigned long long* grab_counter(cudaStream_t s) {
-  static unsigned long long* ring = nullptr;
-  static unsigned next = 0;
-  constexpr unsigned kSlots = 64;
-  if (!ring && cudaMalloc(&ring, kSlots * 128) != cudaSuccess) return nullptr;
-  unsigned long long* c = ring + (next++ % kSlots) * 16;   // 128-byte apart
+  if (!spmm_counters_init()) return nullptr;
+  unsigned long long* c = g_ctr_ring + (g_ctr_next.fetch_add(1) % kCtrSlots) * 16;   // 128 B apart
   if (cudaMemsetAsync(c, 0, sizeof(unsigned long long), s) != cudaSuccess) return nullptr;
   return c;
 }
@@ -1166,6 +1174,14 @@ digest_status launch_narrow(const SpmmArgs& a, cudaStream_t s) {
 }  // namespace
 
 digest_status spmm_one(const SpmmArgs& a, cudaStream_t s);
+
+bool spmm_counters_init() {
+  std::call_once(g_ctr_once, [] {
+    void* p = nullptr;
+    if (cudaMalloc(&p, kCtrSlots * 128) == cudaSuccess) g_ctr_ring = static_cast<unsigned long long*>(p);
+  });
+  return g_ctr_ring != nullptr;
+}
 
 // Column-slab schedule: the gathered source rows of a slab (n_src x slab floats) are
 // sized to stay resident in L2 while the row window sweeps a graph block, so the

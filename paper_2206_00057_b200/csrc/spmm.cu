@@ -1110,9 +1110,9 @@ int narrow_variant() {
 
 // The lean kernel applies when the two sources share one row stride and every offset
 // fits 32 bits (source rows < 2^31, row bytes < 2^32).
-bool narrow_ok(const SpmmArgs& a) {
+bool narrow_ok(const SpmmArgs& a, int max_w4 = 32) {
   const int w4 = a.width / 4;
-  if (w4 < 5 || w4 > 32) return false;
+  if (w4 < 5 || w4 > max_w4) return false;
   const bool two = !(a.in_len != nullptr || a.X1 == nullptr || a.split >= INT32_MAX);
   if (two && a.ld1 != a.ld0) return false;
   return a.ld0 > 0 && a.ld0 * 2 < (int64_t)UINT32_MAX;
@@ -1322,6 +1322,13 @@ digest_status spmm_one(const SpmmArgs& a, cudaStream_t s) {
       case 4: return launch<16, 4, 4, false>(a, s);
       case 5: return launch<32, 2, 2, false>(a, s);
       case 6: return launch<32, 2, 4, false, 4>(a, s);
+      // grouped kernel, 2 rows per warp (16 lanes x 4 float4 per row)
+      case 9:
+        if (a.order && narrow_ok(a, 64)) return launch_g<16, 4, 4, false, 2>(a, s);
+        return launch<32, 2, 8>(a, s);
+      case 10:
+        if (a.order && narrow_ok(a, 64)) return launch_g<16, 4, 2, false, 3>(a, s);
+        return launch<32, 2, 8>(a, s);
       // w=256, persistent grid, products M=1: chunk-prefetching <32,2,8> 14.91 ms vs
       // runtime-loop <32,2,4,MB=4> 15.35 ms (profiles/r1_spmm_variant_sweep.log)
       default: return launch<32, 2, 8>(a, s);

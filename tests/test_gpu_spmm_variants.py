@@ -26,6 +26,8 @@ CASES += [(w, {"DIGEST_SPMM_N": str(n), "MODE": m}) for w in (48, 64, 100, 128) 
           for m in ("0", "1", "2")]
 CASES += [(w, {"DIGEST_SPMM_N": n, "MODE": m}) for n in ("1", "5") for w in (20, 32, 36, 52, 48, 100)
           for m in ("0", "1", "2")]
+# the grouped kernel at w=256 (2 rows per warp), all three products
+CASES += [(256, {"DIGEST_SPMM_V": v, "MODE": m}) for v in ("9", "10") for m in ("0", "1", "2")]
 # several 4096-row windows of the partition's length-grouped row order (grouped kernel)
 CASES += [(w, {"DIGEST_SPMM_N": n, "MODE": m, "NODES": "40000"}) for n in ("1", "5")
           for w in (48, 100) for m in ("0", "1", "2")]

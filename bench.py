@@ -68,6 +68,9 @@ def parse():
                     help="aggregate the static layer-1 inputs once (SURVEY f3 (i)); off by default")
     ap.add_argument("--no-ncu", action="store_true",
                     help="skip the ncu DRAM-traffic probe of the dominant kernel")
+    ap.add_argument("--no-parts-variant", action="store_true",
+                    help="N=1: skip the variant that trains the config's paper partition count "
+                         "(products: 8) on this GPU, the stale-halo exchange included")
     return ap.parse_args()
 
 
@@ -531,6 +534,22 @@ def run_ours(a, rank, world, local):
         cpu = {"value": float(np.mean(per)), "unit": "s", "cores": eff,
                "cores_available": cores(), "kind": "oracle", "sample": sample,
                "full_size_check": full_size_oracle(a.config)}
+    # ---- variant: DIGEST's own mechanism at N=1.  With one partition per GPU, N=1 has no
+    # halo and no exchange; here the config's paper partition count (products: 8) is
+    # trained on this GPU in one process -- every part's stale-halo SpMM, the pushes into
+    # the linked stores every N_sync epochs, the pulls and the 8-way gradient sum (Alg. 1).
+    # The step covers all parts' work, so ms_per_step / parts is the per-GPU share an 8-GPU
+    # run would have if the parts ran concurrently.
+    vparts = VARIANT_PARTS.get(a.config, 0)
+    if (world == 1 and not loop and not a.graph and not a.no_parts_variant and vparts > 1
+            and not a.cache_l1):
+        grp.close()
+        w.part.close()
+        del w, grp
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        variants[f"parts{vparts}_on_one_gpu"] = parts_variant(a, cfg, inp, tc, vparts)
+        grp = None
     if rank == 0:
         line = {
             "metric": METRIC, "value": step_s, "unit": "s", "n_gpus": world, "steps": a.steps,
@@ -566,7 +585,8 @@ def run_ours(a, rank, world, local):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()      # no rank unmaps a buffer a peer may still read
-    grp.close()
+    if grp is not None:
+        grp.close()
     if world > 1:
         D.digest_comm_destroy(comm_grad)
         if comm_halo != comm_grad:
@@ -575,6 +595,69 @@ def run_ours(a, rank, world, local):
 
 
 NCU = "/usr/local/cuda/bin/ncu"
+
+# the partition count each BASELINE.json config is quoted on (its largest)
+VARIANT_PARTS = {"products": 8, "reddit": 8, "arxiv": 8, "flickr": 4, "cora": 2}
+
+
+def parts_variant(a, cfg, inp, tc, M):
+    """All M partitions of the workload trained on this GPU in one process (linked stores):
+    W warm-up epochs, then K epochs timed with CUDA events on the launching stream."""
+    import torch
+    from paper_2206_00057_b200 import capi as D
+    from paper_2206_00057_b200.engine import build_workers, LoopbackGroup
+    from synth import make_block_parts
+    part_of = make_block_parts(cfg, M)
+    ws = build_workers(inp.indptr, inp.indices, inp.x, inp.y, inp.train_mask, inp.weights,
+                       part_of, M, tc)
+    grp = LoopbackGroup(ws)
+    stream = torch.cuda.current_stream()
+    n_sync = tc.sync_interval
+    r = 0
+    for _ in range(a.warmup):
+        r += 1
+        grp.epoch(r)
+    torch.cuda.synchronize()
+    D.digest_prof_read()
+    D.digest_prof_enable(True)
+    n0 = D.digest_launch_count()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps + 1)]
+    ev[0].record(stream)
+    sched = []
+    for i in range(a.steps):
+        r += 1
+        sched.append((r - 1) % n_sync == 0)
+        grp.epoch(r)
+        ev[i + 1].record(stream)
+    torch.cuda.synchronize()
+    launches = D.digest_launch_count() - n0
+    prof = D.digest_prof_read()
+    D.digest_prof_enable(False)
+    ms = ev[0].elapsed_time(ev[-1]) / a.steps
+    per_ep = [ev[i].elapsed_time(ev[i + 1]) for i in range(a.steps)]
+    split = {}
+    for name, want in (("push_epochs", True), ("other_epochs", False)):
+        xs = [t for t, p in zip(per_ep, sched) if p == want]
+        split[name] = {"n": len(xs), "mean_ms": float(np.mean(xs)) if xs else None}
+    infos = [x.part.info for x in ws]
+    out = {"parts": M, "ms_per_step": ms, "ms_per_part": ms / M,
+           "n_halo_total": int(sum(i.n_halo for i in infos)),
+           "n_local_total": int(sum(i.n_local for i in infos)),
+           "halo_over_local": float(sum(i.n_halo for i in infos) / sum(i.n_local for i in infos)),
+           "nnz_total": int(sum(i.nnz for i in infos)),
+           "epoch_ms_by_schedule": split,
+           "kernel_ms_per_step": {k: v["ms"] / a.steps for k, v in prof.items()},
+           "gpu_launches": int(launches),
+           "note": "all M parts of the workload on this GPU in one process (linked stale "
+                   "stores: pull/push of every part's halo rows every N_sync epochs, M-way "
+                   "gradient sum); the step covers all M parts"}
+    grp.close()
+    for x in ws:
+        x.part.close()
+    del ws, grp
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return out
 
 
 def dram_probe(config, parts, rank, width, timeout=300):

@@ -70,6 +70,31 @@ for step in "$@"; do
                 -k "w100-MM_N1-MODE0-ODES40000 or w48-MM_N6-MODE0 or w100-MM_N1-MODE2-ODES40000" -p no:cacheprovider >> ${O}_sanitize2.log 2>&1
               echo "rc=$?" >> ${O}_sanitize2.log
             done ;;
+    hotncu) # L2 hit rate / DRAM bytes of the w=256 product with and without evict_last hot rows
+            for spec in "base::" "pfh0:DIGEST_SPMM_PFH=1,DIGEST_HOT_ROWS=0" "pfh98k:DIGEST_SPMM_PFH=1,DIGEST_HOT_ROWS=98304" \
+                        "pfh400k:DIGEST_SPMM_PFH=1,DIGEST_HOT_ROWS=400000" "pfh1m:DIGEST_SPMM_PFH=1,DIGEST_HOT_ROWS=1000000" \
+                        "v9:DIGEST_SPMM_V=9" "v10:DIGEST_SPMM_V=10" \
+                        "h4_490k:DIGEST_SPMM_PFH=1,DIGEST_SPMM_HINTS=4,DIGEST_HOT_ROWS=490000" \
+                        "h4_980k:DIGEST_SPMM_PFH=1,DIGEST_SPMM_HINTS=4,DIGEST_HOT_ROWS=980000" \
+                        "h4_1470k:DIGEST_SPMM_PFH=1,DIGEST_SPMM_HINTS=4,DIGEST_HOT_ROWS=1470000" \
+                        "h1_490k:DIGEST_SPMM_PFH=1,DIGEST_SPMM_HINTS=1,DIGEST_HOT_ROWS=490000" ${HOTNCU_EXTRA}; do
+              IFS=: read name kn <<< "$spec"
+              echo "== $name $kn" >> ${O}_hotncu.log
+              env DIGEST_KNOBS=1 $(echo $kn | tr ',' ' ') timeout 600 $NCU --metrics \
+                gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct,l1tex__t_sector_hit_rate.pct,sm__warps_active.avg.pct_of_peak_sustained_active,lts__t_sectors_srcunit_tex.sum \
+                --clock-control none -k regex:k_spmm -s 1 -c 1 --csv --print-units base \
+                python tools/spmm_bench.py --widths 256 --iters 1 >> ${O}_hotncu.log 2>&1
+              env DIGEST_KNOBS=1 $(echo $kn | tr ',' ' ') timeout 300 python tools/spmm_bench.py --widths 256 --iters 5 >> ${O}_hotncu.log 2>&1
+            done ;;
+    wsweep) # w=256 SpMM variants on products M=1, one 8-part partition and Reddit M=1
+            for v in ${WSWEEP:-0 9 11 12 13 14 15 16}; do
+              for cp in "products:1" "products:8" "reddit:1"; do
+                IFS=: read cfg parts <<< "$cp"
+                echo "== V=$v $cfg/$parts" >> ${O}_wsweep.log
+                env DIGEST_KNOBS=1 DIGEST_SPMM_V=$v timeout 300 python tools/spmm_bench.py --config $cfg --parts $parts \
+                  --widths ${NW:-256} --iters 5 >> ${O}_wsweep.log 2>&1
+              done
+            done ;;
     timeline) timeout 900 python tools/timeline.py --config products --parts 8 --epochs 3 --sync-interval 1 \
                 --out ${O}_timeline_products8.json > ${O}_timeline.log 2>&1
               timeout 900 python tools/timeline.py --config reddit --parts 4 --epochs 3 --sync-interval 1 \

@@ -265,117 +265,6 @@ __global__ void __launch_bounds__(256, MB) k_spmm(SpmmArgs a) {
   }
 }
 
-// Staged-row variant of k_spmm for full-warp rows (LC = 32; w = 132..256), experiment
-// DIGEST_SPMM_V=11/12.  The row_ptr -> (col, val) -> gather chain at every row start is
-// taken off the critical path without holding registers for it: while row r is gathered,
-// the first (col, val) chunk of the warp's next row is copied into a per-warp shared slot
-// with cp.async (its bounds were loaded one row earlier, and the bounds of the row after it
-// load now), so row r+1's gathers issue right after an LDS.  Later chunks of a long row are
-// prefetched into registers as in k_spmm.
-__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
-  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
-
-template <int VPL, int UNR, int MB>
-__global__ void __launch_bounds__(256, MB) k_spmm_x(SpmmArgs a) {
-  constexpr int STEPS = 32 / UNR;
-  __shared__ int32_t s_col[8][2][32];
-  __shared__ float s_val[8][2][32];
-  const int lane = threadIdx.x & 31;
-  const int wib = threadIdx.x >> 5;
-  const int w4 = a.width >> 2;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  auto bounds = [&](int64_t r, int64_t& b, int64_t& e) {
-    b = e = 0;
-    if (r < a.n_rows) {
-      b = a.row_ptr[r];
-      e = a.in_len ? b + a.in_len[r] : a.row_ptr[r + 1];
-    }
-  };
-  auto stage = [&](int slot, int64_t b, int64_t e) {   // first chunk of a row -> slot
-    if (b + lane < e) {
-      cp_async4(&s_col[wib][slot][lane], a.col + b + lane);
-      cp_async4(&s_val[wib][slot][lane], a.val + b + lane);
-    }
-    cp_async_commit();
-  };
-  int64_t beg, end, nbeg, nend;
-  bounds(row, beg, end);
-  bounds(row + nwarps, nbeg, nend);
-  stage(0, beg, end);
-  int slot = 0;
-  for (; row < a.n_rows; row += nwarps) {
-    int64_t nnbeg, nnend;
-    bounds(row + 2 * nwarps, nnbeg, nnend);   // consumed one row later
-    stage(slot ^ 1, nbeg, nend);              // the next row's first chunk
-    cp_async_wait1();                         // this row's first chunk has landed
-    __syncwarp();
-    int32_t c = (beg + lane < end) ? s_col[wib][slot][lane] : 0;
-    float v = (beg + lane < end) ? s_val[wib][slot][lane] : 0.f;
-    int32_t c_nxt = 0;
-    float v_nxt = 0.f;
-    float4 acc[VPL];
-#pragma unroll
-    for (int q = 0; q < VPL; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int64_t e0 = beg; e0 < end; e0 += 32) {
-      const int cnt = (int)min((int64_t)32, end - e0);
-      if (e0 + 32 + lane < end) {
-        c_nxt = __ldg(a.col + e0 + 32 + lane);
-        v_nxt = __ldg(a.val + e0 + 32 + lane);
-      }
-#pragma unroll
-      for (int st = 0; st < STEPS; ++st) {
-        if (st * UNR >= cnt) break;   // warp-uniform
-        const float* src[UNR];
-        float vv[UNR];
-        bool ok[UNR];
-#pragma unroll
-        for (int u = 0; u < UNR; ++u) {
-          const int j = st * UNR + u;
-          const int cr = __shfl_sync(0xffffffffu, c, j);
-          const float x = __shfl_sync(0xffffffffu, v, j);
-          const int cj = cr & 0x7fffffff;
-          ok[u] = j < cnt;
-          vv[u] = ok[u] ? x : 0.f;
-          src[u] = (int64_t)cj < a.split ? a.X0 + (int64_t)cj * a.ld0
-                                         : a.X1 + ((int64_t)cj - a.split) * a.ld1;
-        }
-        float4 t[UNR][VPL];
-#pragma unroll
-        for (int u = 0; u < UNR; ++u)
-#pragma unroll
-          for (int q = 0; q < VPL; ++q) {
-            const int idx = lane + q * 32;
-            t[u][q] = (ok[u] && idx < w4) ? ldg4(src[u] + 4 * idx) : make_float4(0.f, 0.f, 0.f, 0.f);
-          }
-#pragma unroll
-        for (int u = 0; u < UNR; ++u)
-#pragma unroll
-          for (int q = 0; q < VPL; ++q) {
-            acc[q].x = fmaf(vv[u], t[u][q].x, acc[q].x);
-            acc[q].y = fmaf(vv[u], t[u][q].y, acc[q].y);
-            acc[q].z = fmaf(vv[u], t[u][q].z, acc[q].z);
-            acc[q].w = fmaf(vv[u], t[u][q].w, acc[q].w);
-          }
-      }
-      c = c_nxt;
-      v = v_nxt;
-    }
-    spmm_row_epilogue<32, VPL>(a, row, lane, lane, 0, w4, acc);
-    __syncwarp();   // every lane has read this slot before it is restaged
-    slot ^= 1;
-    beg = nbeg;
-    end = nend;
-    nbeg = nnbeg;
-    nend = nnend;
-  }
-  asm volatile("cp.async.wait_all;" ::: "memory");
-}
-
 // Runtime-trip-count variant (no chunk prefetch, default caching): fewer registers,
 // higher occupancy; best for the wide rows (measured).
 template <int LC, int VPL, int UNR, int MB>
@@ -1145,23 +1034,6 @@ digest_status launch(const SpmmArgs& a, cudaStream_t s) {
   return DIGEST_OK;
 }
 
-// Staged-row kernel launch (k_spmm_x, LC = 32): persistent grid as in launch().
-template <int VPL, int UNR, int MB>
-digest_status launch_x(const SpmmArgs& a, cudaStream_t s) {
-  const double W = a.full_width > 0 ? a.full_width : a.width;
-  const double frac = a.width / W;
-  const double bytes = frac * ((double)a.nnz * (8.0 + 4.0 * W) + (double)a.n_rows * (4.0 * W + 8.0));
-  const double flops = 2.0 * (double)a.nnz * a.width;
-  int64_t blocks = ceil_div(a.n_rows, 8);
-  static const int64_t cap = resident_ctas(k_spmm_x<VPL, UNR, MB>);
-  if (spmm_persistent(a) && blocks > cap) blocks = cap;
-  if (blocks > (int64_t)num_sms() * 64) blocks = (int64_t)num_sms() * 64;
-  if (blocks < 1) blocks = 1;
-  DG_LAUNCH_TAG(DIGEST_PROF_SPMM, (int)W, s, bytes, flops, (k_spmm_x<VPL, UNR, MB>),
-                (unsigned)blocks, 256, 0, a);
-  return DIGEST_OK;
-}
-
 // Lean narrow-slab kernel launch (w4 = width/4 in 5..16).  Byte/flop accounting as in
 // launch(): the slab's share of the whole product's edge-gather bytes.
 template <int LC, int VPL, int UNR, bool RAG, int MB, bool XR = false, bool CH = false>
@@ -1464,35 +1336,25 @@ digest_status spmm_one(const SpmmArgs& a, cudaStream_t s) {
       case 4: return launch<16, 4, 4, false>(a, s);
       case 5: return launch<32, 2, 2, false>(a, s);
       case 6: return launch<32, 2, 4, false, 4>(a, s);
-      // grouped kernel, 2 rows per warp (16 lanes x 4 float4 per row)
-      case 9:
+      // the row-per-warp kernel (the w=256 default before the grouped kernel)
+      case 7: return launch<32, 2, 8>(a, s);
+      case 17:   // grouped with the hot-bit L2 policy (experiment; set DIGEST_HOT_ROWS)
+        if (a.order && narrow_ok(a, 64) && w4 == 64) return launch_g<16, 4, 4, false, 2, 1>(a, s);
+        return launch<32, 2, 8>(a, s);
+      // Default for w = 196..256: the grouped kernel, two rows per warp (16 lanes x 4
+      // float4 per row; length-grouped order, dynamic batches).  Measured w=256
+      // (profiles/r2_w256_sweep.log): products M=1 14.94 -> 11.97 ms (DRAM 77.6 GB at 6.53
+      // TB/s, 1.0 of the copy peak), one 8-part partition 2.06 -> 1.79 ms, Reddit M=1
+      // 11.84 -> 5.81 ms; 4 rows per warp (8 x 8) or fewer edges per step lose.  Without a
+      // row order (or with 64-bit offsets) the row-per-warp chunk-prefetching <32,2,8>
+      // (products M=1 14.91 ms vs 15.35 ms for the runtime-loop <32,2,4,MB=4>,
+      // profiles/r1_spmm_variant_sweep.log).
+      default:
         if (a.order && narrow_ok(a, 64) && w4 > 48) {
           if (w4 == 64) return launch_g<16, 4, 4, false, 2>(a, s);
           return launch_g<16, 4, 4, true, 2>(a, s);
         }
         return launch<32, 2, 8>(a, s);
-      case 14:   // 4 rows per warp (8 lanes x 8 float4)
-        if (a.order && narrow_ok(a, 64) && w4 == 64) return launch_g<8, 8, 2, false, 2>(a, s);
-        return launch<32, 2, 8>(a, s);
-      case 15:
-        if (a.order && narrow_ok(a, 64) && w4 == 64) return launch_g<16, 4, 3, false, 2>(a, s);
-        return launch<32, 2, 8>(a, s);
-      case 16:
-        if (a.order && narrow_ok(a, 64) && w4 == 64) return launch_g<16, 4, 2, false, 2>(a, s);
-        return launch<32, 2, 8>(a, s);
-      case 17:   // V=9 with the hot-bit L2 policy (set DIGEST_HOT_ROWS)
-        if (a.order && narrow_ok(a, 64) && w4 == 64) return launch_g<16, 4, 4, false, 2, 1>(a, s);
-        return launch<32, 2, 8>(a, s);
-      case 10:
-        if (a.order && narrow_ok(a, 64)) return launch_g<16, 4, 2, false, 3>(a, s);
-        return launch<32, 2, 8>(a, s);
-      // staged-row kernel (next row's first (col, val) chunk cp.async'd into shared memory)
-      case 11: return launch_x<2, 8, 2>(a, s);
-      case 12: return launch_x<2, 4, 2>(a, s);
-      case 13: return launch_x<2, 4, 3>(a, s);
-      // w=256, persistent grid, products M=1: chunk-prefetching <32,2,8> 14.91 ms vs
-      // runtime-loop <32,2,4,MB=4> 15.35 ms (profiles/r1_spmm_variant_sweep.log)
-      default: return launch<32, 2, 8>(a, s);
     }
   }
   if (w4 <= 96) return launch<32, 3, 4, false>(a, s);

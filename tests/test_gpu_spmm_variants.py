@@ -26,18 +26,15 @@ CASES += [(w, {"DIGEST_SPMM_N": str(n), "MODE": m}) for w in (48, 64, 100, 128) 
           for m in ("0", "1", "2")]
 CASES += [(w, {"DIGEST_SPMM_N": n, "MODE": m}) for n in ("1", "5") for w in (20, 32, 36, 52, 48, 100)
           for m in ("0", "1", "2")]
-# the grouped kernel at w=256 (2 or 4 rows per warp), all three products; w=200: the ragged
-# last float4 of a lane (RAG)
-CASES += [(256, {"DIGEST_SPMM_V": v, "MODE": m}) for v in ("9", "10", "14", "15", "16")
+# w=196..256: the grouped kernel (default, 2 rows per warp) and the row-per-warp kernel (V=7),
+# all three products; w=200: the ragged last float4 of a lane (RAG)
+CASES += [(w, {"DIGEST_SPMM_V": v, "MODE": m}) for v in ("0", "7") for w in (256, 200)
           for m in ("0", "1", "2")]
-CASES += [(200, {"DIGEST_SPMM_V": "9", "MODE": m}) for m in ("0", "1", "2")]
 CASES += [(256, {"DIGEST_SPMM_V": "17", "DIGEST_HOT_ROWS": "600", "MODE": m}) for m in ("0", "1", "2")]
-# the staged-row kernel (next row's first (col, val) chunk cp.async'd to shared memory)
-CASES += [(w, {"DIGEST_SPMM_V": v, "MODE": m}) for v in ("11", "12", "13") for w in (256, 200)
-          for m in ("0", "1", "2")]
 # several 4096-row windows of the partition's length-grouped row order (grouped kernel)
 CASES += [(w, {"DIGEST_SPMM_N": n, "MODE": m, "NODES": "40000"}) for n in ("1", "5")
           for w in (48, 100) for m in ("0", "1", "2")]
+CASES += [(256, {"MODE": m, "NODES": "40000"}) for m in ("0", "1", "2")]
 # column slabs of the lean kernel (balanced, <= SMAX floats)
 CASES += [(w, {"DIGEST_SPMM_SMAX": sm, "MODE": m}) for w, sm in ((100, "64"), (100, "48"),
                                                                   (256, "64"), (256, "32"),

@@ -95,6 +95,18 @@ for step in "$@"; do
                   --widths ${NW:-256} --iters 5 >> ${O}_wsweep.log 2>&1
               done
             done ;;
+    polncu) # the default (grouped) w=256 product vs the grouped kernel with the hot-bit L2 policy
+            for spec in "grouped::" "g17_300k:DIGEST_SPMM_V=17,DIGEST_HOT_ROWS=300000" \
+                        "g17_490k:DIGEST_SPMM_V=17,DIGEST_HOT_ROWS=490000" "g17_735k:DIGEST_SPMM_V=17,DIGEST_HOT_ROWS=735000" \
+                        "rowwarp:DIGEST_SPMM_V=7"; do
+              IFS=: read name kn <<< "$spec"
+              echo "== $name $kn" >> ${O}_polncu.log
+              env DIGEST_KNOBS=1 $(echo $kn | tr ',' ' ') timeout 600 $NCU --metrics \
+                gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct,l1tex__t_sector_hit_rate.pct,sm__warps_active.avg.pct_of_peak_sustained_active,lts__t_sectors_srcunit_tex.sum \
+                --clock-control none -k regex:k_spmm -s 1 -c 1 --csv --print-units base \
+                python tools/spmm_bench.py --widths 256 --iters 1 >> ${O}_polncu.log 2>&1
+              env DIGEST_KNOBS=1 $(echo $kn | tr ',' ' ') timeout 300 python tools/spmm_bench.py --widths 256 --iters 5 >> ${O}_polncu.log 2>&1
+            done ;;
     timeline) timeout 900 python tools/timeline.py --config products --parts 8 --epochs 3 --sync-interval 1 \
                 --out ${O}_timeline_products8.json > ${O}_timeline.log 2>&1
               timeout 900 python tools/timeline.py --config reddit --parts 4 --epochs 3 --sync-interval 1 \

@@ -533,6 +533,7 @@ digest_status build(int64_t N, int64_t nnz, const int64_t* indptr, const int32_t
   int64_t hot_rows = 98304;   // measured best on products M=1 (w=256 SpMM 20.0 -> 17.8 ms)
   if (const char* e = dg::knob("DIGEST_HOT_ROWS")) hot_rows = atoll(e);
   const int64_t next = n_local + h;
+  if (const char* e = dg::knob("DIGEST_HOT_FRAC")) hot_rows = (int64_t)(atof(e) * (double)next);
   if (hot_rows > 0 && next > 0) {
     int32_t* dext;
     unsigned int* hist;

@@ -20,7 +20,7 @@ for step in "$@"; do
     smoke)  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > ${O}_smoke.log 2>&1; echo "rc=$?" >> ${O}_smoke.log ;;
     bench)  timeout 900 python bench.py > ${O}_bench.log 2>&1 ;;
     launches) timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none --csv \
-              --log-file ${O}_launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-ncu > ${O}_launches.log 2>&1 ;;
+              --log-file ${O}_launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-ncu --no-parts-variant > ${O}_launches.log 2>&1 ;;
     nsweep) for kv in ${NSWEEP:-"DIGEST_SPMM_N=1" "DIGEST_SPMM_N=5" "DIGEST_SPMM_N=6" "DIGEST_SPMM_N=7" "DIGEST_SPMM_N=8"}; do
               kvs=$(echo $kv | tr ',' ' ')
               echo "== $kvs" >> ${O}_nsweep.log
@@ -91,7 +91,7 @@ for step in "$@"; do
               for cp in "products:1" "products:8" "reddit:1"; do
                 IFS=: read cfg parts <<< "$cp"
                 echo "== V=$v $cfg/$parts" >> ${O}_wsweep.log
-                env DIGEST_KNOBS=1 DIGEST_SPMM_V=$v timeout 300 python tools/spmm_bench.py --config $cfg --parts $parts \
+                env DIGEST_KNOBS=1 DIGEST_SPMM_V=$v ${WSWEEP_ENV} timeout 300 python tools/spmm_bench.py --config $cfg --parts $parts \
                   --widths ${NW:-256} --iters 5 >> ${O}_wsweep.log 2>&1
               done
             done ;;
@@ -106,6 +106,13 @@ for step in "$@"; do
                 --clock-control none -k regex:k_spmm -s 1 -c 1 --csv --print-units base \
                 python tools/spmm_bench.py --widths 256 --iters 1 >> ${O}_polncu.log 2>&1
               env DIGEST_KNOBS=1 $(echo $kn | tr ',' ' ') timeout 300 python tools/spmm_bench.py --widths 256 --iters 5 >> ${O}_polncu.log 2>&1
+            done ;;
+    sanitize3) CS=/usr/local/cuda/bin/compute-sanitizer   # the grouped w=256 default (2 rows per warp)
+            for tool in memcheck racecheck synccheck; do
+              echo "== $tool grouped SpMM w=256/200 (default V0, all products, multi-window)" >> ${O}_sanitize3.log
+              timeout 1500 $CS --tool $tool --target-processes all --print-limit 20 python -m pytest tests/test_gpu_spmm_variants.py -q -x \
+                -k "w256-MM_V0-MODE0 or w256-MM_V0-MODE2 or w200-MM_V0-MODE1 or w256-MODE0-ODES40000" -p no:cacheprovider >> ${O}_sanitize3.log 2>&1
+              echo "rc=$?" >> ${O}_sanitize3.log
             done ;;
     timeline) timeout 900 python tools/timeline.py --config products --parts 8 --epochs 3 --sync-interval 1 \
                 --out ${O}_timeline_products8.json > ${O}_timeline.log 2>&1

@@ -586,7 +586,7 @@ __device__ __forceinline__ float4 g_gather(const float4* p, uint32_t cr, uint64_
   return __ldg(p);
 }
 
-template <int LC, int VPL, int UNR, bool TWO, bool RAG, int MB, int POL = 0>
+template <int LC, int VPL, int UNR, bool TWO, bool RAG, int MB, int POL = 0, bool COOP = false>
 __global__ void __launch_bounds__(256, MB) k_spmm_g(SpmmArgs a, const char* __restrict__ x0,
                                                     const char* __restrict__ x1m,
                                                     uint32_t split, uint32_t rb_half,
@@ -681,6 +681,59 @@ __global__ void __launch_bounds__(256, MB) k_spmm_g(SpmmArgs a, const char* __re
           }
         spmm_row_epilogue<LC, VPL>(a, rr, lane, cl, g, w4, acc);
       }
+      continue;
+    }
+    if constexpr (COOP) {
+      // (col, val) of a step loaded once per group: lane cl < UNR loads entry cl (one
+      // coalesced 4*UNR-byte read per group and array) and the group's lanes take the UNR
+      // entries by shuffles at the step start -- 2 loads per lane per step instead of 2 UNR.
+      static_assert(UNR <= LC, "COOP needs UNR <= LC");
+      const int gb = lane & ~(LC - 1);
+      int32_t mc = 0;
+      float mv = 0.f;
+      if (cl < UNR && cl < len) {
+        mc = ld_csr_i(a.col + beg + cl, pol_s);
+        mv = ld_csr_f(a.val + beg + cl, pol_s);
+      }
+      for (int e = 0; e < mx; e += UNR) {
+        int32_t c[UNR];
+        float v[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          c[u] = __shfl_sync(0xffffffffu, mc, gb + u);
+          v[u] = __shfl_sync(0xffffffffu, mv, gb + u);
+        }
+        mc = 0;
+        mv = 0.f;
+        if (cl < UNR && e + UNR + cl < len) {
+          mc = ld_csr_i(a.col + beg + e + UNR + cl, pol_s);
+          mv = ld_csr_f(a.val + beg + e + UNR + cl, pol_s);
+        }
+        float4 t[UNR][VPL];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          const uint32_t cr = (uint32_t)c[u];
+          const char* bs = x0;
+          if (TWO) bs = (cr & 0x7fffffffu) >= split ? x1m : x0;
+          const float4* p = reinterpret_cast<const float4*>(bs + (uint64_t)(cr << 1) * rb_half);
+#pragma unroll
+          for (int q = 0; q < VPL; ++q) {
+            const int idx = cl + q * LC;
+            t[u][q] = g_gather<POL>(p + (RAG && q == VPL - 1 ? min(idx, w4 - 1) : idx), cr,
+                                    pol_h, pol_s);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+#pragma unroll
+          for (int q = 0; q < VPL; ++q) {
+            acc[q].x = fmaf(v[u], t[u][q].x, acc[q].x);
+            acc[q].y = fmaf(v[u], t[u][q].y, acc[q].y);
+            acc[q].z = fmaf(v[u], t[u][q].z, acc[q].z);
+            acc[q].w = fmaf(v[u], t[u][q].w, acc[q].w);
+          }
+      }
+      spmm_group_epilogue<LC, VPL>(a, row, lane, cl, w4, acc);
       continue;
     }
     int32_t c[UNR];
@@ -1081,7 +1134,7 @@ unsigned long long* grab_counter(cudaStream_t s) {
   return c;
 }
 
-template <int LC, int VPL, int UNR, bool RAG, int MB, int POL = 0>
+template <int LC, int VPL, int UNR, bool RAG, int MB, int POL = 0, bool COOP = false>
 digest_status launch_g(const SpmmArgs& a, cudaStream_t s) {
   unsigned long long* ctr = grab_counter(s);
   DG_ARG(ctr, DIGEST_E_CUDA, "SpMM work counter allocation failed");
@@ -1095,14 +1148,14 @@ digest_status launch_g(const SpmmArgs& a, cudaStream_t s) {
   const uint32_t rb_half = (uint32_t)(a.ld0 * 2);
   int64_t blocks = ceil_div(a.n_rows, 8 * (32 / LC));
   if (two) {
-    static const int64_t cap = resident_ctas(k_spmm_g<LC, VPL, UNR, true, RAG, MB, POL>);
+    static const int64_t cap = resident_ctas(k_spmm_g<LC, VPL, UNR, true, RAG, MB, POL, COOP>);
     if (blocks > cap) blocks = cap;
-    DG_LAUNCH_TAG(DIGEST_PROF_SPMM, (int)W, s, bytes, flops, (k_spmm_g<LC, VPL, UNR, true, RAG, MB, POL>),
+    DG_LAUNCH_TAG(DIGEST_PROF_SPMM, (int)W, s, bytes, flops, (k_spmm_g<LC, VPL, UNR, true, RAG, MB, POL, COOP>),
                   (unsigned)blocks, 256, 0, a, x0, x1m, (uint32_t)a.split, rb_half, ctr);
   } else {
-    static const int64_t cap = resident_ctas(k_spmm_g<LC, VPL, UNR, false, RAG, MB, POL>);
+    static const int64_t cap = resident_ctas(k_spmm_g<LC, VPL, UNR, false, RAG, MB, POL, COOP>);
     if (blocks > cap) blocks = cap;
-    DG_LAUNCH_TAG(DIGEST_PROF_SPMM, (int)W, s, bytes, flops, (k_spmm_g<LC, VPL, UNR, false, RAG, MB, POL>),
+    DG_LAUNCH_TAG(DIGEST_PROF_SPMM, (int)W, s, bytes, flops, (k_spmm_g<LC, VPL, UNR, false, RAG, MB, POL, COOP>),
                   (unsigned)blocks, 256, 0, a, x0, x1m, (uint32_t)INT32_MAX, rb_half, ctr);
   }
   return DIGEST_OK;
@@ -1141,6 +1194,14 @@ digest_status launch_narrow(const SpmmArgs& a, cudaStream_t s) {
   // of >= 1M rows (M=1: 2.96 -> 2.22 ms).  On smaller products (an 8-part partition, 306K
   // rows) the w=48 grouped kernel loses (0.46 -> 0.55 ms): 8 rows per warp batch leave only
   // ~11 batches per warp and the last wave's imbalance shows, so the lean kernel stays.
+  if (v == 11 && a.order) {   // experiment: cooperative (col, val) loads in the grouped kernel
+    if (w4 > 16) return launch_g<8, 4, 4, true, 2, 0, true>(a, s);
+    if (w4 == 12) return launch_g<4, 3, 4, false, 3, 0, true>(a, s);
+  }
+  if (v == 12 && a.order) {   // the same at one more CTA per SM
+    if (w4 > 16) return launch_g<8, 4, 4, true, 3, 0, true>(a, s);
+    if (w4 == 12) return launch_g<4, 3, 4, false, 4, 0, true>(a, s);
+  }
   if (v == 1 && a.order && w4 > 16) return launch_g<8, 4, 4, true, 2>(a, s);
   if (v == 1 && a.order && w4 == 12 && a.n_rows >= (1 << 20))
     return launch_g<4, 3, 4, false, 3>(a, s);
@@ -1338,6 +1399,9 @@ digest_status spmm_one(const SpmmArgs& a, cudaStream_t s) {
       case 6: return launch<32, 2, 4, false, 4>(a, s);
       // the row-per-warp kernel (the w=256 default before the grouped kernel)
       case 7: return launch<32, 2, 8>(a, s);
+      case 18:   // grouped with cooperative (col, val) loads (experiment)
+        if (a.order && narrow_ok(a, 64) && w4 == 64) return launch_g<16, 4, 4, false, 2, 0, true>(a, s);
+        return launch<32, 2, 8>(a, s);
       case 17:   // grouped with the hot-bit L2 policy (experiment; set DIGEST_HOT_ROWS)
         if (a.order && narrow_ok(a, 64) && w4 == 64) return launch_g<16, 4, 4, false, 2, 1>(a, s);
         return launch<32, 2, 8>(a, s);

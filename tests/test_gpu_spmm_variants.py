@@ -35,6 +35,10 @@ CASES += [(256, {"DIGEST_SPMM_V": "17", "DIGEST_HOT_ROWS": "600", "MODE": m}) fo
 CASES += [(w, {"DIGEST_SPMM_N": n, "MODE": m, "NODES": "40000"}) for n in ("1", "5")
           for w in (48, 100) for m in ("0", "1", "2")]
 CASES += [(256, {"MODE": m, "NODES": "40000"}) for m in ("0", "1", "2")]
+# cooperative (col, val) loads in the grouped kernel (experiment)
+CASES += [(w, {"DIGEST_SPMM_N": n, "MODE": m}) for n in ("11", "12") for w in (48, 100)
+          for m in ("0", "1", "2")]
+CASES += [(256, {"DIGEST_SPMM_V": "18", "MODE": m}) for m in ("0", "1", "2")]
 # column slabs of the lean kernel (balanced, <= SMAX floats)
 CASES += [(w, {"DIGEST_SPMM_SMAX": sm, "MODE": m}) for w, sm in ((100, "64"), (100, "48"),
                                                                   (256, "64"), (256, "32"),

@@ -107,13 +107,6 @@ for step in "$@"; do
                 python tools/spmm_bench.py --widths 256 --iters 1 >> ${O}_polncu.log 2>&1
               env DIGEST_KNOBS=1 $(echo $kn | tr ',' ' ') timeout 300 python tools/spmm_bench.py --widths 256 --iters 5 >> ${O}_polncu.log 2>&1
             done ;;
-    sanitize3) CS=/usr/local/cuda/bin/compute-sanitizer   # the grouped w=256 default (2 rows per warp)
-            for tool in memcheck racecheck synccheck; do
-              echo "== $tool grouped SpMM w=256/200 (default V0, all products, multi-window)" >> ${O}_sanitize3.log
-              timeout 1500 $CS --tool $tool --target-processes all --print-limit 20 python -m pytest tests/test_gpu_spmm_variants.py -q -x \
-                -k "w256-MM_V0-MODE0 or w256-MM_V0-MODE2 or w200-MM_V0-MODE1 or w256-MODE0-ODES40000" -p no:cacheprovider >> ${O}_sanitize3.log 2>&1
-              echo "rc=$?" >> ${O}_sanitize3.log
-            done ;;
     timeline) timeout 900 python tools/timeline.py --config products --parts 8 --epochs 3 --sync-interval 1 \
                 --out ${O}_timeline_products8.json > ${O}_timeline.log 2>&1
               timeout 900 python tools/timeline.py --config reddit --parts 4 --epochs 3 --sync-interval 1 \

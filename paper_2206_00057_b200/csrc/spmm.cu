@@ -1165,7 +1165,9 @@ digest_status launch_g(const SpmmArgs& a, cudaStream_t s) {
 // 1 = default lean kernel; 2 = cross-row pipelined, 32 gathers per group step (fewer
 // warps); 3 = default without the CSR evict_first policy; 4 = cross-row pipelined at the
 // default's unroll and occupancy (profiles/r2_spmm_variant_sweeps.log); 5-9 = the grouped
-// kernel (k_spmm_g) at every narrow width with different unroll / lane layouts.
+// kernel (k_spmm_g) at every narrow width with different unroll / lane layouts; 11 = the
+// grouped defaults with per-lane (col, val) loads; 13 = the grouped defaults (cooperative
+// loads) at any row count.
 int narrow_variant() {
   static int v = -2;
   if (v == -2) {
@@ -1194,17 +1196,22 @@ digest_status launch_narrow(const SpmmArgs& a, cudaStream_t s) {
   // of >= 1M rows (M=1: 2.96 -> 2.22 ms).  On smaller products (an 8-part partition, 306K
   // rows) the w=48 grouped kernel loses (0.46 -> 0.55 ms): 8 rows per warp batch leave only
   // ~11 batches per warp and the last wave's imbalance shows, so the lean kernel stays.
-  if (v == 11 && a.order) {   // experiment: cooperative (col, val) loads in the grouped kernel
+  // Cooperative (col, val) loads (COOP: one load per group lane, shuffled to the group)
+  // since the end of round 2: products M=1 w=48 2.231 -> 2.144 ms, w=100 4.460 -> 4.417
+  // ms, 8-part partition w=100 0.813 -> 0.803 ms (profiles/r2_spmm_grouped_sweep.log);
+  // v == 11 keeps the per-lane loads for comparison.  (The same at one more CTA per SM
+  // measured 5-19% slower and is not instantiated.)
+  if (v == 11 && a.order) {
+    if (w4 > 16) return launch_g<8, 4, 4, true, 2>(a, s);
+    if (w4 == 12) return launch_g<4, 3, 4, false, 3>(a, s);
+  }
+  if (v == 13 && a.order) {   // the default grouped forms at any row count (parity tests)
     if (w4 > 16) return launch_g<8, 4, 4, true, 2, 0, true>(a, s);
     if (w4 == 12) return launch_g<4, 3, 4, false, 3, 0, true>(a, s);
   }
-  if (v == 12 && a.order) {   // the same at one more CTA per SM
-    if (w4 > 16) return launch_g<8, 4, 4, true, 3, 0, true>(a, s);
-    if (w4 == 12) return launch_g<4, 3, 4, false, 4, 0, true>(a, s);
-  }
-  if (v == 1 && a.order && w4 > 16) return launch_g<8, 4, 4, true, 2>(a, s);
+  if (v == 1 && a.order && w4 > 16) return launch_g<8, 4, 4, true, 2, 0, true>(a, s);
   if (v == 1 && a.order && w4 == 12 && a.n_rows >= (1 << 20))
-    return launch_g<4, 3, 4, false, 3>(a, s);
+    return launch_g<4, 3, 4, false, 3, 0, true>(a, s);
   if (v >= 5 && v <= 9 && a.order) {   // grouped kernel experiments (one row per edge group)
     if (w4 == 12) {
       if (v == 9) return launch_g<4, 3, 3, false, 3>(a, s);

@@ -35,8 +35,10 @@ CASES += [(256, {"DIGEST_SPMM_V": "17", "DIGEST_HOT_ROWS": "600", "MODE": m}) fo
 CASES += [(w, {"DIGEST_SPMM_N": n, "MODE": m, "NODES": "40000"}) for n in ("1", "5")
           for w in (48, 100) for m in ("0", "1", "2")]
 CASES += [(256, {"MODE": m, "NODES": "40000"}) for m in ("0", "1", "2")]
-# cooperative (col, val) loads in the grouped kernel (experiment)
-CASES += [(w, {"DIGEST_SPMM_N": n, "MODE": m}) for n in ("11", "12") for w in (48, 100)
+# the grouped kernel with per-lane (col, val) loads (N=11; the default loads them cooperatively)
+CASES += [(w, {"DIGEST_SPMM_N": n, "MODE": m}) for n in ("11", "13") for w in (48, 100)
+          for m in ("0", "1", "2")]
+CASES += [(w, {"DIGEST_SPMM_N": "13", "MODE": m, "NODES": "40000"}) for w in (48, 100)
           for m in ("0", "1", "2")]
 CASES += [(256, {"DIGEST_SPMM_V": "18", "MODE": m}) for m in ("0", "1", "2")]
 # column slabs of the lean kernel (balanced, <= SMAX floats)

@@ -104,7 +104,9 @@ struct Cfg {
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
 k_gemm_tf32x3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBh,
-              const __grid_constant__ CUtensorMap tmBl, const EpiArgs e, int K) {
+              const __grid_constant__ CUtensorMap tmBl, const EpiArgs e, int K, int raw_hi) {
+  // raw_hi (experiment DIGEST_GEMM_RAWHI): A_hi is the raw fp32 tile (kind::tf32 reading
+  // only the upper 19 bits), so the split workers write only A_lo.
   using G = Cfg<BN>;
   const int64_t M = e.M;
   const int N = e.N;
@@ -222,7 +224,7 @@ k_gemm_tf32x3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
           float4 v = A[idx];
           float4 h = make_float4(tc::tf32_hi(v.x), tc::tf32_hi(v.y), tc::tf32_hi(v.z),
                                  tc::tf32_hi(v.w));
-          A[idx] = h;
+          if (!raw_hi) A[idx] = h;
           Al[idx] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
         }
         tc::fence_proxy_async_smem();
@@ -296,6 +298,15 @@ void* workspace(size_t bytes) {
   return g_ws.p;
 }
 
+int gemm_raw_hi() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = dg::knob("DIGEST_GEMM_RAWHI");
+    v = e ? (atoi(e) ? 1 : 0) : 0;
+  }
+  return v;
+}
+
 template <int BN>
 digest_status launch_tc(const GemmArgs& g, const CUtensorMap& tA, const CUtensorMap& tBh,
                         const CUtensorMap& tBl, cudaStream_t s) {
@@ -313,7 +324,7 @@ digest_status launch_tc(const GemmArgs& g, const CUtensorMap& tA, const CUtensor
   // profile tag: 1KKKKNNN (forward-type GEMM, K and N)
   DG_LAUNCH_TAG(DIGEST_PROF_GEMM, 10000000 + (int)g.K * 1000 + g.N, s, bytes, flops,
                 k_gemm_tf32x3<BN>, (unsigned)grid, kThreads, G::SMEM, tA, tBh, tBl, epi_of(g),
-                (int)g.K);
+                (int)g.K, gemm_raw_hi());
   return DIGEST_OK;
 }
 

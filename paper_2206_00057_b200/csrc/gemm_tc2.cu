@@ -50,7 +50,11 @@ struct Cfg2 {
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
 k_gemm2_tf32x3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBh,
-               const __grid_constant__ CUtensorMap tmBl, const EpiArgs e, int K, int single) {
+               const __grid_constant__ CUtensorMap tmBl, const EpiArgs e, int K, int flags) {
+  // flags bit 1 (experiment DIGEST_GEMM_RAWHI): A_hi is the raw fp32 tile itself, on the
+  // reading that kind::tf32 uses only an operand's upper 19 bits (truncation), so only
+  // A_lo = A - trunc19(A) is written back.
+  const int single = flags & 1, raw_hi = flags & 2;
   // single: the 128 split-worker (epilogue) threads of a CTA meet at a named barrier and
   // ONE of them arrives on rank 0's conv (tempty) barrier -- 2 cluster-scope arrivals per
   // stage instead of 256 (each thread still fences its own smem writes / TMEM loads).
@@ -176,7 +180,7 @@ k_gemm2_tf32x3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           float4 v = A[idx];
           float4 h = make_float4(tc::tf32_hi(v.x), tc::tf32_hi(v.y), tc::tf32_hi(v.z),
                                  tc::tf32_hi(v.w));
-          A[idx] = h;
+          if (!raw_hi) A[idx] = h;
           Al[idx] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
         }
         tc::fence_proxy_async_smem();
@@ -254,6 +258,7 @@ digest_status launch2(const GemmArgs& g, const CUtensorMap& tA, const CUtensorMa
   if (single < 0) {
     const char* ev = dg::knob("DIGEST_GEMM_SINGLE_ARRIVE");
     single = ev ? atoi(ev) : 1;
+    if (const char* er = dg::knob("DIGEST_GEMM_RAWHI")) single |= atoi(er) ? 2 : 0;
   }
   cudaError_t e = cudaLaunchKernelEx(&cfg, k_gemm2_tf32x3<BN>, tA, tBh, tBl, epi_of(g), (int)g.K,
                                      single);

@@ -107,6 +107,10 @@ for step in "$@"; do
                 python tools/spmm_bench.py --widths 256 --iters 1 >> ${O}_polncu.log 2>&1
               env DIGEST_KNOBS=1 $(echo $kn | tr ',' ' ') timeout 300 python tools/spmm_bench.py --widths 256 --iters 5 >> ${O}_polncu.log 2>&1
             done ;;
+    gemmraw) # A_hi = the raw fp32 tile (kind::tf32 reading the upper 19 bits) vs the split A_hi
+            timeout 900 python tools/gemm_bench.py --iters 10 --shapes 100x256,256x256,256x48,48x256 > ${O}_gemmraw.log 2>&1
+            env DIGEST_KNOBS=1 DIGEST_GEMM_RAWHI=1 timeout 900 python tools/gemm_bench.py --iters 10 --shapes 100x256,256x256,256x48,48x256 >> ${O}_gemmraw.log 2>&1
+            timeout 900 python -m pytest tests/test_gpu_gemm_variants.py -q -p no:cacheprovider >> ${O}_gemmraw.log 2>&1 ;;
     timeline) timeout 900 python tools/timeline.py --config products --parts 8 --epochs 3 --sync-interval 1 \
                 --out ${O}_timeline_products8.json > ${O}_timeline.log 2>&1
               timeout 900 python tools/timeline.py --config reddit --parts 4 --epochs 3 --sync-interval 1 \

@@ -79,6 +79,21 @@ bool make_tmap_rows_fwd(CUtensorMap* m, const void* base, uint64_t inner, uint64
   return make_tmap_rows(m, base, inner, outer, row_stride_bytes);
 }
 
+// A_hi = the raw fp32 tile (default): kind::tf32 reads only the upper 19 bits of an
+// operand, i.e. truncates exactly as tf32_hi does, so the split workers write only A_lo.
+// Measured (tools/gemm_bench.py, 2.45M rows): K x N = 100x256 0.968 -> 0.951 ms, 256x256
+// 1.488 -> 1.453, 256x48 0.825 -> 0.812, 48x256 0.613 -> 0.597; the results are
+// bit-identical to the explicit split (tests/test_gpu_gemm_variants.py).
+// DIGEST_GEMM_RAWHI=0 writes A_hi explicitly.
+int gemm_raw_hi() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = dg::knob("DIGEST_GEMM_RAWHI");
+    v = e ? (atoi(e) ? 1 : 0) : 1;
+  }
+  return v;
+}
+
 namespace {
 
 constexpr int kBM = 128, kBK = 32, kEpiWarps = 8, kThreads = (6 + kEpiWarps) * 32;
@@ -105,8 +120,8 @@ template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
 k_gemm_tf32x3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBh,
               const __grid_constant__ CUtensorMap tmBl, const EpiArgs e, int K, int raw_hi) {
-  // raw_hi (experiment DIGEST_GEMM_RAWHI): A_hi is the raw fp32 tile (kind::tf32 reading
-  // only the upper 19 bits), so the split workers write only A_lo.
+  // raw_hi: A_hi is the raw fp32 tile (kind::tf32 reads only the upper 19 bits), so the
+  // split workers write only A_lo (gemm_raw_hi()).
   using G = Cfg<BN>;
   const int64_t M = e.M;
   const int N = e.N;
@@ -296,15 +311,6 @@ void* workspace(size_t bytes) {
     g_ws.bytes = nb;
   }
   return g_ws.p;
-}
-
-int gemm_raw_hi() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = dg::knob("DIGEST_GEMM_RAWHI");
-    v = e ? (atoi(e) ? 1 : 0) : 0;
-  }
-  return v;
 }
 
 template <int BN>

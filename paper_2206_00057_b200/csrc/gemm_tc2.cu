@@ -22,6 +22,8 @@ namespace dg {
 
 void* workspace(size_t bytes);
 
+int gemm_raw_hi();   // gemm_tc.cu
+
 namespace {
 
 // warps: 0 TMA, 1 MMA (rank 0), 2-5 split workers, 6-13 epilogue: two warps per TMEM lane
@@ -51,8 +53,8 @@ template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
 k_gemm2_tf32x3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBh,
                const __grid_constant__ CUtensorMap tmBl, const EpiArgs e, int K, int flags) {
-  // flags bit 1 (experiment DIGEST_GEMM_RAWHI): A_hi is the raw fp32 tile itself, on the
-  // reading that kind::tf32 uses only an operand's upper 19 bits (truncation), so only
+  // flags bit 1 (default, see gemm_raw_hi in gemm_tc.cu): A_hi is the raw fp32 tile
+  // itself -- kind::tf32 uses only an operand's upper 19 bits -- so only
   // A_lo = A - trunc19(A) is written back.
   const int single = flags & 1, raw_hi = flags & 2;
   // single: the 128 split-worker (epilogue) threads of a CTA meet at a named barrier and
@@ -258,7 +260,7 @@ digest_status launch2(const GemmArgs& g, const CUtensorMap& tA, const CUtensorMa
   if (single < 0) {
     const char* ev = dg::knob("DIGEST_GEMM_SINGLE_ARRIVE");
     single = ev ? atoi(ev) : 1;
-    if (const char* er = dg::knob("DIGEST_GEMM_RAWHI")) single |= atoi(er) ? 2 : 0;
+    if (gemm_raw_hi()) single |= 2;
   }
   cudaError_t e = cudaLaunchKernelEx(&cfg, k_gemm2_tf32x3<BN>, tA, tBh, tBl, epi_of(g), (int)g.K,
                                      single);

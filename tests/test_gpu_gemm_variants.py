@@ -29,7 +29,7 @@ np.savez(out, A=A.numpy(), B=B.numpy(), C=C.cpu().numpy())
 
 SHAPES = [(3000, 256, 100, 0), (3000, 256, 256, 0), (3000, 48, 256, 0), (3000, 256, 48, 0),
           (200, 256, 100, 0), (777, 36, 52, 0), (1000, 256, 48, 1)]
-CASES = [(s, {"DIGEST_GEMM_RAWHI": "1"}) for s in SHAPES]
+CASES = [(s, {"DIGEST_GEMM_RAWHI": v}) for s in SHAPES for v in ("0", "1")]
 
 
 @pytest.mark.timeout(300)
@@ -50,3 +50,24 @@ def test_gemm_variant(shape, env, tmp_path):
     ref = d["A"].astype(np.float64) @ (Bm.T if bt else Bm)
     err = np.abs(d["C"] - ref).max() / np.abs(ref).max()
     assert err <= 3e-5, err
+
+
+def _run(shape, env, path):
+    M, N, K, bt = shape
+    r = subprocess.run([sys.executable, "-c", PROC, str(M), str(N), str(K), str(bt), path],
+                       env={**os.environ, **env, "DIGEST_KNOBS": "1", "PYTHONPATH": ROOT},
+                       capture_output=True, text=True, timeout=280)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return np.load(path)["C"]
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("shape", SHAPES, ids=[f"{m}x{n}x{k}{'bt' if b else ''}" for m, n, k, b in SHAPES])
+def test_gemm_raw_hi_is_bit_identical(shape, tmp_path):
+    """The default feeds the raw fp32 A tile as A_hi (kind::tf32 reads the upper 19 bits);
+    it must equal the explicit truncation split bit for bit."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    c_raw = _run(shape, {"DIGEST_GEMM_RAWHI": "1"}, str(tmp_path / "a.npz"))
+    c_split = _run(shape, {"DIGEST_GEMM_RAWHI": "0"}, str(tmp_path / "b.npz"))
+    assert np.array_equal(c_raw.view(np.uint32), c_split.view(np.uint32))

@@ -78,12 +78,14 @@ k_xent64(const float* __restrict__ Z, int64_t n, int C, int64_t ld, const int32_
   float z0 = -INFINITY, z1 = -INFINITY;
   int yi = 0;
   bool t = false;
+  // A row outside the training mask only gets its zero gradient row, so its logits are
+  // not read (products: 8% of the rows train -- the logits read drops by 92%).
   auto load = [&](int64_t i) {
     const float* z = Z + i * ld;
-    z0 = c0 ? __ldg(z + lane) : -INFINITY;
-    z1 = c1 ? __ldg(z + lane + 32) : -INFINITY;
-    yi = __ldg(y + i);
     t = __ldg(mask + i) != 0;
+    yi = __ldg(y + i);
+    z0 = (c0 && t) ? __ldg(z + lane) : -INFINITY;
+    z1 = (c1 && t) ? __ldg(z + lane + 32) : -INFINITY;
   };
   if (warp < n) load(warp);
   for (int64_t i = warp; i < n; i += nw) {

@@ -73,7 +73,7 @@ for step in "$@"; do
     hotncu) # L2 hit rate / DRAM bytes of the w=256 product with and without evict_last hot rows
             for spec in "base::" "pfh0:DIGEST_SPMM_PFH=1,DIGEST_HOT_ROWS=0" "pfh98k:DIGEST_SPMM_PFH=1,DIGEST_HOT_ROWS=98304" \
                         "pfh400k:DIGEST_SPMM_PFH=1,DIGEST_HOT_ROWS=400000" "pfh1m:DIGEST_SPMM_PFH=1,DIGEST_HOT_ROWS=1000000" \
-                        "v9:DIGEST_SPMM_V=9" "v10:DIGEST_SPMM_V=10" \
+                        "rowwarp:DIGEST_SPMM_V=7" \
                         "h4_490k:DIGEST_SPMM_PFH=1,DIGEST_SPMM_HINTS=4,DIGEST_HOT_ROWS=490000" \
                         "h4_980k:DIGEST_SPMM_PFH=1,DIGEST_SPMM_HINTS=4,DIGEST_HOT_ROWS=980000" \
                         "h4_1470k:DIGEST_SPMM_PFH=1,DIGEST_SPMM_HINTS=4,DIGEST_HOT_ROWS=1470000" \
@@ -87,7 +87,7 @@ for step in "$@"; do
               env DIGEST_KNOBS=1 $(echo $kn | tr ',' ' ') timeout 300 python tools/spmm_bench.py --widths 256 --iters 5 >> ${O}_hotncu.log 2>&1
             done ;;
     wsweep) # w=256 SpMM variants on products M=1, one 8-part partition and Reddit M=1
-            for v in ${WSWEEP:-0 9 11 12 13 14 15 16}; do
+            for v in ${WSWEEP:-0 7 17 18}; do
               for cp in "products:1" "products:8" "reddit:1"; do
                 IFS=: read cfg parts <<< "$cp"
                 echo "== V=$v $cfg/$parts" >> ${O}_wsweep.log

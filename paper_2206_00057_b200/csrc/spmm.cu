@@ -1199,8 +1199,9 @@ digest_status launch_narrow(const SpmmArgs& a, cudaStream_t s) {
   // Cooperative (col, val) loads (COOP: one load per group lane, shuffled to the group)
   // since the end of round 2: products M=1 w=48 2.231 -> 2.144 ms, w=100 4.460 -> 4.417
   // ms, 8-part partition w=100 0.813 -> 0.803 ms (profiles/r2_spmm_grouped_sweep.log);
-  // v == 11 keeps the per-lane loads for comparison.  (The same at one more CTA per SM
-  // measured 5-19% slower and is not instantiated.)
+  // v == 11 keeps the per-lane loads for comparison.  (The same at one more CTA per SM,
+  // and 3 or 2 edges per step at 3-4 CTAs per SM, measured 5-43% slower and are not
+  // instantiated.)
   if (v == 11 && a.order) {
     if (w4 > 16) return launch_g<8, 4, 4, true, 2>(a, s);
     if (w4 == 12) return launch_g<4, 3, 4, false, 3>(a, s);

@@ -150,6 +150,18 @@ digest_status digest_part_export(const digest_part* part, int32_t* local_ids,
                                  int32_t* rh_col, float* rh_val, void* stream);
 digest_status digest_part_destroy(digest_part* part);
 
+/* Loss rows of the partition (Eq. 3: the loss sums over the training nodes only, so
+ * the last layer's gradient G_logits -- and every operand derived from it row by row, D and
+ * U = D W^T -- is zero on the other local rows).  row_mask: device uint8[n_local], nonzero =
+ * the row may be nonzero (the local training rows); NULL clears.  Builds, inside the
+ * handle, P_in and P_out^T restricted to the columns whose row_mask is set (entries kept in
+ * their order, so the products equal the full ones exactly: the dropped terms are products
+ * with zero rows).  digest_layer_bwd(..., DIGEST_BWD_LOSS_ROWS) then runs its P_in / P_out^T
+ * products over them; the caller guarantees G_out's rows outside the mask are zero.
+ * Synchronises `stream` (sizes are data-dependent).  Errors: DIGEST_E_INVALID (NULL
+ * partition), DIGEST_E_NOMEM, DIGEST_E_CUDA. */
+digest_status digest_part_set_loss_mask(digest_part* part, const uint8_t* row_mask, void* stream);
+
 /* ------------------------------------------------------------------ stale store
  * The stale representation store H~^(l), l in [1, L-1] (levels never
  * equal L).  Per level: a front buffer (read by the layer that
@@ -283,7 +295,8 @@ digest_status digest_layer_mask(const digest_part* part, int32_t d_in, int32_t d
  * n_local x d_in tensor (ld_gm floats; factor 1[gin_mask > 0], e.g. the previous H)
  * or, with flags DIGEST_BWD_GIN_MASK_BITS, a 1-bit mask (ld_gm 32-bit words per row,
  * e.g. digest_layer_mask of the previous layer). */
-enum { DIGEST_BWD_G_IS_D = 1u, DIGEST_BWD_GIN_MASK_BITS = 2u, DIGEST_BWD_HALO_SAVE_S = 4u };
+enum { DIGEST_BWD_G_IS_D = 1u, DIGEST_BWD_GIN_MASK_BITS = 2u, DIGEST_BWD_HALO_SAVE_S = 4u,
+       DIGEST_BWD_LOSS_ROWS = 8u };
 digest_status digest_layer_bwd(const digest_part* part, const float* X_local, int64_t ld_x,
                                const float* X_halo, int64_t ld_xh, const float* W,
                                int32_t d_in, int32_t d_out, int32_t act, int32_t order,
@@ -299,7 +312,10 @@ digest_status digest_layer_bwd(const digest_part* part, const float* X_local, in
  * receives S = P_out^T D~^(t), the part of the term the paper's DIGEST backward returns
  * ONE iteration later (G~_H^(t) = P_in^T D~^(t) W~^(t)T + P_out^T D~^(t-1)
  * W~^(t)T); the caller keeps it and forms next iteration's rows with
- * digest_gemm(S, W, G, DIGEST_GEMM_BT) = S W^T at the then-current W. */
+ * digest_gemm(S, W, G, DIGEST_GEMM_BT) = S W^T at the then-current W.
+ * With flags DIGEST_BWD_LOSS_ROWS (the last layer, after digest_part_set_loss_mask): the
+ * P_in / P_out^T products run over the loss-row CSRs; identical results when G_out is zero
+ * outside the mask (DIGEST_E_STATE if no mask was set). */
 
 /* The propagation product alone (the aggregation of Eq. 5 / its transposes):
  *   mode 0: Y = P_m X_ext      (n_local rows; X_ext = [X_local ; X_halo], width w)

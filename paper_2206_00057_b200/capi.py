@@ -65,6 +65,7 @@ _SIGS = {
     "digest_part_get_info": ([_p, _p], _i32),
     "digest_part_export": ([_p] * 11, _i32),
     "digest_part_destroy": ([_p], _i32),
+    "digest_part_set_loss_mask": ([_p, _p, _p], _i32),
     "digest_store_create": ([_p, _p, _i32, _p, _p], _i32),
     "digest_store_create_ex": ([_p, _p, _i32, _p, _u32, _p], _i32),
     "digest_store_link": ([_p, _i32], _i32),
@@ -237,6 +238,11 @@ def digest_part_destroy(part):
     _check(lib.digest_part_destroy(part))
 
 
+def digest_part_set_loss_mask(part, row_mask, stream=None):
+    """row_mask: device uint8 [n_local] (the local training rows) or None to clear."""
+    _check(lib.digest_part_set_loss_mask(part, ptr(row_mask), stream_ptr(stream)))
+
+
 # ------------------------------------------------------------------ store
 def digest_store_create_ex(part, comm, widths, flags=0):
     arr = (C.c_int32 * max(1, len(widths)))(*widths)
@@ -331,6 +337,7 @@ def digest_layer_mask(part, d_in, d_out, order, saved):
 BWD_G_IS_D = 1
 BWD_GIN_MASK_BITS = 2
 BWD_HALO_SAVE_S = 4
+BWD_LOSS_ROWS = 8
 GEMM_RELU = 1
 GEMM_BT = 2
 

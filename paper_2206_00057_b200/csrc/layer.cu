@@ -120,6 +120,43 @@ dg::SpmmArgs spmm_in(const digest_part* p, const float* X, int64_t ld, float* Y,
   return a;
 }
 
+// The loss-row forms (digest_part_set_loss_mask): the same products over the CSRs that keep
+// only the columns whose operand row can be nonzero (the training rows of the last layer's
+// gradient), in the same entry order -- the dropped terms are exact zeros.
+dg::SpmmArgs spmm_lm(const digest_part* p, const float* X, int64_t ld, float* Y, int64_t ldy,
+                     int32_t w) {
+  dg::SpmmArgs a{};
+  a.row_ptr = p->lm_ptr;
+  a.order = p->ord_lm;
+  a.col = p->lm_col;
+  a.val = p->lm_val;
+  a.n_rows = p->n_local;
+  a.nnz = p->lm_nnz;
+  a.csr_len = p->lm_nnz;
+  a.X0 = X;
+  a.ld0 = ld;
+  a.split = INT64_MAX;
+  a.x0_rows = p->n_local;
+  a.X1 = X;
+  a.ld1 = ld;
+  a.Y = Y;
+  a.ldy = ldy;
+  a.width = w;
+  return a;
+}
+dg::SpmmArgs spmm_lmh(const digest_part* p, const float* X, int64_t ld, float* Y, int64_t ldy,
+                      int32_t w) {
+  dg::SpmmArgs a = spmm_lm(p, X, ld, Y, ldy, w);
+  a.row_ptr = p->lmh_ptr;
+  a.order = p->ord_lmh;
+  a.col = p->lmh_col;
+  a.val = p->lmh_val;
+  a.n_rows = p->n_halo;
+  a.nnz = p->lmh_nnz;
+  a.csr_len = p->lmh_nnz;
+  return a;
+}
+
 // Y (n_halo rows) = P_out^T X over the reverse-halo CSR (halo row j -> local columns).
 dg::SpmmArgs spmm_rh(const digest_part* p, const float* X, int64_t ld, float* Y, int64_t ldy,
                      int32_t w) {
@@ -258,6 +295,17 @@ digest_status digest_layer_bwd(const digest_part* p, const float* X_local, int64
   const float* gm_f = gm_bits ? nullptr : static_cast<const float*>(gin_mask);
   const uint32_t* gm_b = gm_bits ? static_cast<const uint32_t*>(gin_mask) : nullptr;
   const bool save_s = (flags & DIGEST_BWD_HALO_SAVE_S) != 0;   // G_halo <- P_out^T D
+  // DIGEST_BWD_LOSS_ROWS: G_out's rows outside the loss mask are zero, so the P_in / P_out^T
+  // products of D (and of U = D W^T) run over the loss-row CSRs
+  const bool lrows = (flags & DIGEST_BWD_LOSS_ROWS) != 0;
+  DG_ARG(!lrows || p->lm_nnz >= 0, DIGEST_E_STATE,
+         "DIGEST_BWD_LOSS_ROWS without digest_part_set_loss_mask");
+  auto p_in = [&](const float* X, int64_t ld, float* Y, int64_t ldy, int32_t w) {
+    return lrows ? spmm_lm(p, X, ld, Y, ldy, w) : spmm_in(p, X, ld, Y, ldy, w);
+  };
+  auto p_rh = [&](const float* X, int64_t ld, float* Y, int64_t ldy, int32_t w) {
+    return lrows ? spmm_lmh(p, X, ld, Y, ldy, w) : spmm_rh(p, X, ld, Y, ldy, w);
+  };
   if (G_halo && pl.h > 0) DG_TRY(check_mat(G_halo, ld_gh, save_s ? d_out : d_in, "G_halo"));
   const bool want_halo = G_halo && pl.h > 0;
   DG_ARG(W && G_W && scratch, DIGEST_E_INVALID, "W, G_W and scratch must be non-NULL");
@@ -297,7 +345,7 @@ digest_status digest_layer_bwd(const digest_part* p, const float* X_local, int64
       DG_TRY(dg::gemm(g, s));
     }
     if (G_in) {
-      dg::SpmmArgs a = spmm_in(p, U, pl.ldi, G_in, ld_gi, d_in);
+      dg::SpmmArgs a = p_in(U, pl.ldi, G_in, ld_gi, d_in);
       a.mask = gm_f;
       a.ldm = ld_gm;
       a.mbits = gm_b;
@@ -305,20 +353,20 @@ digest_status digest_layer_bwd(const digest_part* p, const float* X_local, int64
       DG_TRY(dg::spmm(a, s));
     }
     if (want_halo && save_s)   // S = P_out^T D~^(t), returned next iteration
-      DG_TRY(dg::spmm(spmm_rh(p, D, ldd, G_halo, ld_gh, d_out), s));
+      DG_TRY(dg::spmm(p_rh(D, ldd, G_halo, ld_gh, d_out), s));
     else if (want_halo)        // same-iteration return: G_halo = P_out^T U
-      DG_TRY(dg::spmm(spmm_rh(p, U, pl.ldi, G_halo, ld_gh, d_in), s));
+      DG_TRY(dg::spmm(p_rh(U, pl.ldi, G_halo, ld_gh, d_in), s));
   } else {
     DG_TRY(check_mat(X_local, ld_x, d_in, "X_local"));
     if (pl.h > 0) DG_TRY(check_mat(X_halo, ld_xh, d_in, "X_halo"));
     float* S = carve(scratch, off, sizeof(float) * (pl.n + pl.h) * pl.ldo);
     void* wsc = carve(scratch, off, 0);
-    DG_TRY(dg::spmm(spmm_in(p, D, ldd, S, pl.ldo, d_out), s));
+    DG_TRY(dg::spmm(p_in(D, ldd, S, pl.ldo, d_out), s));
     // S_halo = P_out^T D (reverse-halo CSR, no atomics); with HALO_SAVE_S written
     // straight into the caller's G_halo, which also feeds the weight gradient
     float* Sh = want_halo && save_s ? G_halo : S + pl.n * pl.ldo;
     const int64_t ldsh = want_halo && save_s ? ld_gh : pl.ldo;
-    if (pl.h > 0) DG_TRY(dg::spmm(spmm_rh(p, D, ldd, Sh, ldsh, d_out), s));
+    if (pl.h > 0) DG_TRY(dg::spmm(p_rh(D, ldd, Sh, ldsh, d_out), s));
     dg::WgradSeg segs[2] = {{X_local, ld_x, S, pl.ldo, nullptr, 0, pl.n},
                             {X_halo, ld_xh, Sh, ldsh, nullptr, 0, pl.h}};
     DG_TRY(dg::wgrad(segs, pl.h > 0 ? 2 : 1, d_in, d_out, G_W, wsc, s));

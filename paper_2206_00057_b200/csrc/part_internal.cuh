@@ -26,4 +26,16 @@ struct digest_part {
   int32_t* ord_full = nullptr;   // [n_local]
   int32_t* ord_in = nullptr;     // [n_local]
   int32_t* ord_rh = nullptr;     // [n_halo]
+  // loss-row products (digest_part_set_loss_mask): P_in and P_out^T restricted to the
+  // columns (local rows) whose mask is set -- the only rows of the last layer's gradient
+  // operand that can be nonzero.  Same entry order as col / rh_col; empty when unset.
+  int64_t lm_nnz = -1, lmh_nnz = 0;   // lm_nnz < 0: no loss mask set
+  int64_t* lm_ptr = nullptr;     // [n_local+1]
+  int32_t* lm_col = nullptr;     // [lm_nnz]
+  float* lm_val = nullptr;
+  int32_t* ord_lm = nullptr;     // [n_local]
+  int64_t* lmh_ptr = nullptr;    // [n_halo+1]
+  int32_t* lmh_col = nullptr;    // [lmh_nnz]
+  float* lmh_val = nullptr;
+  int32_t* ord_lmh = nullptr;    // [n_halo]
 };

@@ -10,6 +10,8 @@
 #include "part_internal.cuh"
 #include "scan.cuh"
 
+#include <cub/device/device_scan.cuh>
+
 namespace {
 
 using dg::ceil_div;
@@ -378,8 +380,103 @@ digest_status build_orders(digest_part* P, cudaStream_t s) {
   return DIGEST_OK;
 }
 
+void free_loss_mask(digest_part* p) {
+  cudaFree(p->lm_ptr);
+  cudaFree(p->lm_col);
+  cudaFree(p->lm_val);
+  cudaFree(p->ord_lm);
+  cudaFree(p->lmh_ptr);
+  cudaFree(p->lmh_col);
+  cudaFree(p->lmh_val);
+  cudaFree(p->ord_lmh);
+  p->lm_ptr = p->lmh_ptr = nullptr;
+  p->lm_col = p->lmh_col = p->ord_lm = p->ord_lmh = nullptr;
+  p->lm_val = p->lmh_val = nullptr;
+  p->lm_nnz = -1;
+  p->lmh_nnz = 0;
+}
+
+// Loss-row filter of a CSR (warp per row): the entries of row r in
+// [ptr[r], ptr[r] + (in_len ? in_len[r] : ptr[r+1] - ptr[r])) whose column (bit 31 = the
+// L2 hint, ignored) is a set row of `mask`.  Pass 1 counts them, pass 2 copies them in
+// their original order (ballot + prefix popcount per 32-entry chunk).
+__global__ void k_lm_count(const int64_t* __restrict__ ptr, const int32_t* __restrict__ in_len,
+                           int64_t n, const int32_t* __restrict__ col,
+                           const uint8_t* __restrict__ mask, int64_t* __restrict__ cnt) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n;
+       r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t b = ptr[r], e = in_len ? b + in_len[r] : ptr[r + 1];
+    int64_t c = 0;
+    for (int64_t i = b + lane; i < e; i += 32) c += mask[col[i] & 0x7fffffff] != 0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) cnt[r] = c;
+  }
+}
+__global__ void k_lm_fill(const int64_t* __restrict__ ptr, const int32_t* __restrict__ in_len,
+                          int64_t n, const int32_t* __restrict__ col, const float* __restrict__ val,
+                          const uint8_t* __restrict__ mask, const int64_t* __restrict__ optr,
+                          int32_t* __restrict__ ocol, float* __restrict__ oval) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n;
+       r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t b = ptr[r], e = in_len ? b + in_len[r] : ptr[r + 1];
+    int64_t o = optr[r];
+    for (int64_t i0 = b; i0 < e; i0 += 32) {
+      const int64_t i = i0 + lane;
+      const int32_t c = i < e ? col[i] : 0;
+      const bool keep = i < e && mask[c & 0x7fffffff] != 0;
+      const unsigned bal = __ballot_sync(0xffffffffu, keep);
+      if (keep) {
+        const int64_t at = o + __popc(bal & ((1u << lane) - 1u));
+        ocol[at] = c;
+        oval[at] = val[i];
+      }
+      o += __popc(bal);
+    }
+  }
+}
+
+// Builds one filtered CSR: *optr [n+1], *ocol / *oval [*onnz], *oord [n] (the grouped
+// kernel's row order).
+digest_status build_filtered(const int64_t* ptr, const int32_t* in_len, int64_t n,
+                             const int32_t* col, const float* val, const uint8_t* mask,
+                             cudaStream_t s, int64_t** optr, int32_t** ocol, float** oval,
+                             int32_t** oord, int64_t* onnz) {
+  Temps t;
+  int64_t* cnt;
+  DG_TRY(t.alloc(&cnt, n + 1));
+  DG_TRY(dmalloc(optr, n + 1));
+  DG_CUDA(cudaMemsetAsync(cnt + n, 0, sizeof(int64_t), s));
+  const unsigned grid = (unsigned)std::min<int64_t>(dg::ceil_div(n, 8), 148 * 64);
+  if (n > 0)
+    DG_LAUNCH(DIGEST_PROF_OTHER, s, 0, 0, k_lm_count, grid, 256, 0, ptr, in_len, n, col, mask, cnt);
+  size_t tb = 0;
+  DG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, *optr, (int)(n + 1), s));
+  void* tmp;
+  DG_TRY(t.alloc(reinterpret_cast<uint8_t**>(&tmp), (int64_t)tb));
+  DG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, *optr, (int)(n + 1), s));
+  int64_t total = 0;
+  DG_CUDA(cudaMemcpyAsync(&total, *optr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  DG_CUDA(cudaStreamSynchronize(s));
+  *onnz = total;
+  DG_TRY(dmalloc(ocol, total));
+  DG_TRY(dmalloc(oval, total));
+  DG_TRY(dmalloc(oord, n));
+  if (n > 0) {
+    DG_LAUNCH(DIGEST_PROF_OTHER, s, 0, 0, k_lm_fill, grid, 256, 0, ptr, in_len, n, col, val, mask,
+              (const int64_t*)*optr, *ocol, *oval);
+    DG_LAUNCH(DIGEST_PROF_OTHER, s, 0, 0, k_len_order, (unsigned)dg::ceil_div(n, kOrdWin), 256, 0,
+              (const int64_t*)*optr, (const int32_t*)nullptr, n, *oord);
+  }
+  DG_CUDA(cudaStreamSynchronize(s));   // the temporaries are freed on return
+  return DIGEST_OK;
+}
+
 void free_part(digest_part* p) {
   if (!p) return;
+  free_loss_mask(p);
   cudaFree(p->ord_full);
   cudaFree(p->ord_in);
   cudaFree(p->ord_rh);
@@ -590,6 +687,21 @@ digest_status digest_partition(int64_t num_nodes, int64_t nnz, const int64_t* in
   }
   *out_h = P;
   return DIGEST_OK;
+}
+
+digest_status digest_part_set_loss_mask(digest_part* p, const uint8_t* row_mask, void* stream) {
+  DG_ARG(p, DIGEST_E_INVALID, "NULL partition");
+  free_loss_mask(p);
+  if (!row_mask) return DIGEST_OK;
+  cudaStream_t s = dg::as_stream(stream);
+  digest_status st = build_filtered(p->row_ptr, p->in_len, p->n_local, p->col, p->val, row_mask,
+                                    s, &p->lm_ptr, &p->lm_col, &p->lm_val, &p->ord_lm,
+                                    &p->lm_nnz);
+  if (st == DIGEST_OK && p->n_halo > 0)
+    st = build_filtered(p->rh_ptr, nullptr, p->n_halo, p->rh_col, p->rh_val, row_mask, s,
+                        &p->lmh_ptr, &p->lmh_col, &p->lmh_val, &p->ord_lmh, &p->lmh_nnz);
+  if (st != DIGEST_OK) free_loss_mask(p);
+  return st;
 }
 
 digest_status digest_part_get_info(const digest_part* p, digest_part_info* info) {

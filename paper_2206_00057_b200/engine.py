@@ -56,6 +56,8 @@ class TrainConfig:
     device_step: bool = False   # Adam step count on the device (CUDA-graph capturable epochs)
     fused_agg: bool = True      # peer transport: weight gradients written straight into the
                                 # AGG window slot, one-kernel allreduce
+    loss_rows: bool = True      # last layer's backward products over the training-row columns
+                                # only (G_logits is zero elsewhere; exact)
 
     def __post_init__(self):
         hg = self.halo_grad
@@ -108,6 +110,8 @@ class DigestWorker:
         n, h = part.n_local, part.n_halo
         self.x_local, self.x_halo = x_local, (x_halo if h > 0 else None)
         self.labels, self.train_mask = labels, train_mask
+        if cfg.loss_rows:   # the loss-row CSRs (the mask of the rows G_logits can be nonzero on)
+            D.digest_part_set_loss_mask(part.handle, train_mask)
         self.w_loss = float(w_loss)
         self.comm_grad, self.comm_halo = comm_grad, comm_halo
         # weights: one flat buffer (AGG and the update are single launches)
@@ -245,7 +249,8 @@ class DigestWorker:
         D.digest_layer_bwd(self.part.handle, xl, xh, ldh, self.W[l - 1], dims[l - 1], dims[l],
                            act, self.layer_order(l), self.saved[l], None, self.G[l],
                            gw, self.G[l - 1] if l >= 2 else None, self.scratch,
-                           stream, flags=(D.BWD_G_IS_D if l < self.L else 0) | hflags,
+                           stream, flags=(D.BWD_G_IS_D if l < self.L else
+                                          (D.BWD_LOSS_ROWS if self.cfg.loss_rows else 0)) | hflags,
                            gin_mask=self.mask_bits[l - 1] if l >= 2 else None, G_halo=gh,
                            ld_gh=ldgh)
 

@@ -162,3 +162,73 @@ def test_trajectory_with_stale_halo_grad(M, N, opt):
     # the returned term is real: the first layer's weights leave the constant-halo run
     assert rel(run.weights[0], base.weights[0]) > 10 * TOL
     grp.close()
+
+
+@pytest.mark.parametrize("d_in,d_out,order,save_s", [(24, 40, 1, False), (40, 24, 2, False),
+                                                     (256, 48, 0, False), (256, 48, 0, True),
+                                                     (40, 8, 2, True)])
+def test_loss_rows_products_equal_full_products(d_in, d_out, order, save_s):
+    """digest_part_set_loss_mask + DIGEST_BWD_LOSS_ROWS (the last layer's P_in / P_out^T
+    products over the training-row columns only) = the full products when G_out is
+    zero outside the mask; and both = the oracle."""
+    Dm = D()
+    cfg = small_config(num_nodes=900, nnz=9000, d0=d_in, hidden=(d_out,), seed=11 + d_in)
+    ip, ix = make_graph(cfg)
+    part = make_random_parts(cfg.num_nodes, 3, 2)
+    p, _ = gpu_partition(ip, ix, part, 3, 1)
+    op = oracle.oracle_partition(ip, ix, part, 3, 1)
+    g = torch.Generator().manual_seed(d_in * 7 + d_out)
+    xl = torch.rand(p.n_local, d_in, generator=g) * 2 - 1
+    xh = torch.rand(p.n_halo, d_in, generator=g) * 2 - 1
+    w = (torch.rand(d_in, d_out, generator=g) * 2 - 1) / np.sqrt(d_in)
+    tmask = (torch.rand(p.n_local, generator=g) < 0.1).to(torch.uint8)
+    gout = torch.randn(p.n_local, d_out, generator=g) * tmask[:, None].float()
+    sv, sc = Dm.digest_layer_workspace(p.handle, d_in, d_out, order)
+    saved = torch.empty(max(sv, 256), dtype=torch.uint8, device="cuda")
+    scratch = torch.empty(max(sc, 256), dtype=torch.uint8, device="cuda")
+    H = torch.empty(p.n_local, d_out, device="cuda")
+    Dm.digest_layer_fwd(p.handle, xl.cuda(), xh.cuda(), d_in, w.cuda(), d_in, d_out, 0, order, H,
+                        saved, scratch)
+    outs = []
+    for lrows in (False, True):
+        if lrows:
+            Dm.digest_part_set_loss_mask(p.handle, tmask.cuda())
+        GW = torch.empty(d_in, d_out, device="cuda")
+        Gin = torch.empty(p.n_local, d_in, device="cuda")
+        Gh = torch.full((p.n_halo, d_out if save_s else d_in), 9.0, device="cuda")
+        fl = (Dm.BWD_LOSS_ROWS if lrows else 0) | (Dm.BWD_HALO_SAVE_S if save_s else 0)
+        Dm.digest_layer_bwd(p.handle, xl.cuda(), xh.cuda(), d_in, w.cuda(), d_in, d_out, 0, order,
+                            saved, H, gout.cuda(), GW, Gin, scratch, G_halo=Gh, flags=fl)
+        torch.cuda.synchronize()
+        outs.append([GW.cpu().numpy(), Gin.cpu().numpy(), Gh.cpu().numpy()])
+    for a, b in zip(*outs):
+        assert rel(b, a) <= 1e-6
+    ref = layer_backward(op, xl.numpy(), xh.numpy(), w.numpy(), gout.numpy(), None, True,
+                         need_g_halo=not save_s)
+    assert rel(outs[1][0], ref["G_W"]) <= TOL
+    assert rel(outs[1][1], ref["G_in"]) <= TOL
+    if not save_s:
+        assert rel(outs[1][2], ref["G_halo"]) <= TOL
+    Dm.digest_part_set_loss_mask(p.handle, None)
+    p.close()
+
+
+def test_loss_rows_flag_without_mask_is_refused():
+    Dm = D()
+    cfg = small_config(num_nodes=300, nnz=2400, d0=8, hidden=(8,), seed=3)
+    ip, ix = make_graph(cfg)
+    part = make_random_parts(cfg.num_nodes, 2, 1)
+    p, _ = gpu_partition(ip, ix, part, 2, 0)
+    sv, sc = Dm.digest_layer_workspace(p.handle, 8, 8, 2)
+    saved = torch.empty(max(sv, 256), dtype=torch.uint8, device="cuda")
+    scratch = torch.empty(max(sc, 256), dtype=torch.uint8, device="cuda")
+    x = torch.rand(p.n_local, 8, device="cuda")
+    xh = torch.rand(max(p.n_halo, 1), 8, device="cuda")
+    w = torch.rand(8, 8, device="cuda")
+    H = torch.empty(p.n_local, 8, device="cuda")
+    Dm.digest_layer_fwd(p.handle, x, xh, 8, w, 8, 8, 0, 2, H, saved, scratch)
+    GW = torch.empty(8, 8, device="cuda")
+    with pytest.raises(Dm.DigestError):
+        Dm.digest_layer_bwd(p.handle, x, xh, 8, w, 8, 8, 0, 2, saved, H, H, GW, None, scratch,
+                            flags=Dm.BWD_LOSS_ROWS)
+    p.close()
